@@ -1,0 +1,355 @@
+// kernels.cuh -- the __global__ kernels of libqapsa (sm_100a).
+//
+//   k_reset          p <- source, best_p <- p, C <- Eq.(1), best <- C   (qap_reset / qap_create)
+//   k_cost           Eq.(1) of a permutation (qap_cost)
+//   k_delta_init     step (a), Δ for all pairs, one thread per pair  (qap_delta_init)
+//   k_sa_chain       persistent single-chain kernel, 1 CTA           (qap_sa_run)
+//   k_ensemble       persistent multi-chain kernel, G chains / CTA   (qap_ensemble_run)
+//   k_ens_reduce     argmin over chains + summed statistics
+//   k_delta_bounds   min nonzero |Δ|, max |Δ| for the schedule rule R2 (qap_schedule_bounds)
+//
+// Citation keys: P:n = PAPER.md line n, R# = DESIGN.md readings.
+#pragma once
+#include <cstdint>
+
+#include "chain.cuh"
+
+namespace qapsa {
+
+struct DevState {                 // single-chain scalars, device resident
+    long long cost;
+    long long best_cost;
+    unsigned long long digest;
+    unsigned long long accepted;  // cumulative since reset
+    unsigned int near_count;      // cumulative since reset (= log entries, may exceed cap)
+    unsigned int pad;
+};
+
+struct ChainResult {              // mirrors qap_chain_result
+    long long cost, best_cost;
+    unsigned long long accepted, near_ties, digest, iterations;
+};
+
+// ---------------- shared-memory layout of one chain group ----------------
+struct GroupLayout {
+    int bp, d, dab, p, bestp, slots, flags, bytes;
+};
+__host__ __device__ inline int align16(int x) { return (x + 15) & ~15; }
+__host__ __device__ inline GroupLayout group_layout(int n, int ld, int M, int tb_bytes, int nw,
+                                                    bool d_in_smem) {
+    GroupLayout L;
+    int o = 0;
+    L.bp = o;    o = align16(o + n * ld * tb_bytes);
+    L.d = o;     o = align16(o + (d_in_smem ? M * 4 : 0));
+    L.dab = o;   o = align16(o + n * 8);
+    L.p = o;     o = align16(o + n * 2);
+    L.bestp = o; o = align16(o + n * 2);
+    L.slots = o; o = align16(o + 2 * nw * 16);
+    L.flags = o; o = align16(o + 4 * 4);
+    L.bytes = o;
+    return L;
+}
+
+template <typename TA, typename TB>
+__device__ inline ChainSmem<TA, TB> group_view(unsigned char* base, const GroupLayout& L,
+                                               int32_t* d_global) {
+    ChainSmem<TA, TB> cs;
+    cs.Bp = reinterpret_cast<TB*>(base + L.bp);
+    cs.D = d_global ? d_global : reinterpret_cast<int32_t*>(base + L.d);
+    cs.dAB = reinterpret_cast<int2*>(base + L.dab);
+    cs.p = reinterpret_cast<uint16_t*>(base + L.p);
+    cs.best_p = reinterpret_cast<uint16_t*>(base + L.bestp);
+    cs.slots = reinterpret_cast<int4*>(base + L.slots);
+    cs.flags = reinterpret_cast<int*>(base + L.flags);
+    return cs;
+}
+
+// cooperative copy of bytes (16-byte aligned, size multiple of 4)
+__device__ inline void copy_words(void* dst, const void* src, int bytes, int t, int nt) {
+    const int n16 = bytes >> 4;
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+    const uint4* s4 = reinterpret_cast<const uint4*>(src);
+    for (int i = t; i < n16; i += nt) d4[i] = s4[i];
+    uint32_t* d1 = reinterpret_cast<uint32_t*>(dst);
+    const uint32_t* s1 = reinterpret_cast<const uint32_t*>(src);
+    for (int i = (n16 << 2) + t; i < (bytes >> 2); i += nt) d1[i] = s1[i];
+}
+
+// B'_ij = B_{p(i),p(j)} into shared memory; columns >= n zero.
+template <typename TB>
+__device__ inline void build_bprime(TB* Bp, const TB* __restrict__ B, const uint16_t* p, int n,
+                                    int ld, int t, int nt) {
+    for (int idx = t; idx < n * ld; idx += nt) {
+        const int i = idx / ld, j = idx - i * ld;
+        Bp[idx] = j < n ? B[p[i] * ld + p[j]] : (TB)0;
+    }
+}
+
+// ---------------- small kernels ----------------
+
+template <typename TA, typename TB>
+__global__ void k_reset(const TA* __restrict__ A, const TB* __restrict__ B, const int32_t* src, int n,
+                        int ld, int32_t* p, int32_t* best_p, DevState* st) {
+    __shared__ long long part[32];
+    const int t = threadIdx.x;
+    long long acc = 0;
+    for (int idx = t; idx < n * n; idx += blockDim.x) {
+        const int i = idx / n, j = idx - i * n;
+        acc += (long long)A[i * ld + j] * (long long)B[src[i] * ld + src[j]];
+    }
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((t & 31) == 0) part[t >> 5] = acc;
+    __syncthreads();
+    for (int i = t; i < n; i += blockDim.x) {
+        const int32_t v = src[i];
+        p[i] = v;
+        best_p[i] = v;
+    }
+    if (t == 0) {
+        long long c = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) c += part[w];
+        st->cost = c;
+        st->best_cost = c;
+        st->digest = kDigestSeed;
+        st->accepted = 0;
+        st->near_count = 0;
+    }
+}
+
+template <typename TA, typename TB>
+__global__ void k_cost(const TA* __restrict__ A, const TB* __restrict__ B, const int32_t* perm, int n,
+                       int ld, long long* out) {
+    __shared__ long long part[32];
+    const int t = threadIdx.x;
+    long long acc = 0;
+    for (int idx = t; idx < n * n; idx += blockDim.x) {
+        const int i = idx / n, j = idx - i * n;
+        acc += (long long)A[i * ld + j] * (long long)B[perm[i] * ld + perm[j]];
+    }
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((t & 31) == 0) part[t >> 5] = acc;
+    __syncthreads();
+    if (t == 0) {
+        long long c = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) c += part[w];
+        *out = c;
+    }
+}
+
+// Step (a): one thread per pair, B' read through p (gather from L2).
+// δ(r,s) = 2 [ sum_all k (a_rk - a_sk)(B'_sk - B'_rk) + 2 a_rs B'_rs ]
+template <typename TA, typename TB>
+__global__ void k_delta_init(const TA* __restrict__ A, const TB* __restrict__ B,
+                             const int32_t* __restrict__ p, int n, int ld, int M, int32_t* D) {
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < M; q += gridDim.x * blockDim.x) {
+        int r, s;
+        tri_pair(n, q, &r, &s);
+        const TA* Ar = A + r * ld;
+        const TA* As = A + s * ld;
+        const TB* Br = B + p[r] * ld;
+        const TB* Bs = B + p[s] * ld;
+        int acc = 0;
+        for (int k = 0; k < n; ++k) {
+            const int pk = __ldg(p + k);
+            acc += ((int)Ar[k] - (int)As[k]) * ((int)Bs[pk] - (int)Br[pk]);
+        }
+        D[q] = 2 * (acc + 2 * (int)Ar[s] * (int)Br[p[s]]);
+    }
+}
+
+__global__ void k_delta_bounds(const int32_t* __restrict__ D, int M, int* out /* [0]=dmin, [1]=dmax */) {
+    __shared__ int smin[32], smax[32];
+    int mn = INT_MAX, mx = 0;
+    for (int q = threadIdx.x; q < M; q += blockDim.x) {
+        const int a = abs(D[q]);
+        mx = max(mx, a);
+        if (a) mn = min(mn, a);
+    }
+    mn = __reduce_min_sync(0xffffffffu, mn);
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if ((threadIdx.x & 31) == 0) { smin[threadIdx.x >> 5] = mn; smax[threadIdx.x >> 5] = mx; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) { mn = min(mn, smin[w]); mx = max(mx, smax[w]); }
+        out[0] = mn == INT_MAX ? 0 : mn;
+        out[1] = mx;
+    }
+}
+
+// ---------------- the persistent single-chain kernel (qap_sa_run) ----------------
+struct ChainArgs {
+    const void* A;           // n x ld compact
+    const void* B;           // n x ld compact
+    int32_t* p;              // n
+    int32_t* best_p;         // n
+    int32_t* D;              // M (global copy; also the working Δ when !D_SMEM)
+    DevState* st;
+    unsigned int* near_count;
+    unsigned long long* near_k;
+    unsigned char* near_dec;
+    int near_cap;
+    int n, ld, M, wmax;
+    unsigned long long k0, k_end, seed;
+    Sched sch;
+};
+
+template <typename TA, typename TB, int NT, bool D_SMEM>
+__global__ void __launch_bounds__(NT, 1) k_sa_chain(const ChainArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int t = threadIdx.x;
+    const int n = a.n, ld = a.ld, M = a.M;
+    const int a_bytes = align16(n * ld * (int)sizeof(TA));
+    TA* As = reinterpret_cast<TA*>(smem);
+    const GroupLayout L = group_layout(n, ld, M, sizeof(TB), NT / 32, D_SMEM);
+    ChainSmem<TA, TB> cs = group_view<TA, TB>(smem + a_bytes, L, D_SMEM ? nullptr : a.D);
+
+    copy_words(As, a.A, n * ld * (int)sizeof(TA), t, NT);
+    for (int i = t; i < n; i += NT) {
+        cs.p[i] = (uint16_t)a.p[i];
+        cs.best_p[i] = (uint16_t)a.best_p[i];
+    }
+    if (D_SMEM) copy_words(cs.D, a.D, M * 4, t, NT);
+    if (t < 4) cs.flags[t] = 0;
+    __syncthreads();
+    build_bprime(cs.Bp, reinterpret_cast<const TB*>(a.B), cs.p, n, ld, t, NT);
+    ChainScalars io{a.st->cost, a.st->best_cost, a.st->digest};
+    __syncthreads();
+
+    const NearSink sink{a.near_count, a.near_k, a.near_dec, a.near_cap};
+    const uint64_t acc = chain_run<TA, TB, NT>(As, cs, n, ld, M, a.k0, a.k_end, a.sch, a.seed, 0u,
+                                               0, t, a.wmax, io, sink);
+
+    for (int i = t; i < n; i += NT) {
+        a.p[i] = cs.p[i];
+        a.best_p[i] = cs.best_p[i];
+    }
+    if (D_SMEM) copy_words(a.D, cs.D, M * 4, t, NT);
+    if (t == 0) {
+        a.st->cost = io.cost;
+        a.st->best_cost = io.best;
+        a.st->digest = io.digest;
+        a.st->accepted += acc;
+    }
+}
+
+// ---------------- the persistent ensemble kernel (qap_ensemble_run) ----------------
+struct EnsArgs {
+    const void* A;
+    const void* B;
+    const int32_t* p0s;          // count x n
+    ChainResult* res;            // count
+    uint16_t* best_perms;        // count x n
+    unsigned int* next_chain;    // work counter
+    int count, n, ld, M, wmax;
+    unsigned int chain_begin;
+    unsigned long long iters, seed;
+    Sched sch;
+};
+
+template <typename TA, typename TB, int NT>
+__global__ void __launch_bounds__(1024, 1) k_ensemble(const EnsArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int n = a.n, ld = a.ld, M = a.M;
+    const int a_bytes = align16(n * ld * (int)sizeof(TA));
+    TA* As = reinterpret_cast<TA*>(smem);
+    const GroupLayout L = group_layout(n, ld, M, sizeof(TB), NT / 32, true);
+    const int g = threadIdx.x / NT, t = threadIdx.x % NT, bar = 1 + g;
+    ChainSmem<TA, TB> cs = group_view<TA, TB>(smem + a_bytes + g * L.bytes, L, nullptr);
+
+    copy_words(As, a.A, n * ld * (int)sizeof(TA), threadIdx.x, blockDim.x);
+    __syncthreads();
+
+    for (;;) {
+        if (t == 0) cs.flags[2] = (int)atomicAdd(a.next_chain, 1u);
+        group_sync(bar, NT);
+        const int ci = cs.flags[2];
+        if (ci >= a.count) break;
+        const int32_t* p0 = a.p0s + (size_t)ci * n;
+        for (int i = t; i < n; i += NT) {
+            cs.p[i] = (uint16_t)p0[i];
+            cs.best_p[i] = (uint16_t)p0[i];
+        }
+        if (t < 2) cs.flags[t] = 0;
+        group_sync(bar, NT);
+        build_bprime(cs.Bp, reinterpret_cast<const TB*>(a.B), cs.p, n, ld, t, NT);
+        group_sync(bar, NT);
+        chain_delta_init<TA, TB, NT>(As, cs, n, ld, M, t);
+        // C = Eq.(1) = sum_ij A_ij B'_ij
+        long long part = 0;
+        for (int idx = t; idx < n * n; idx += NT) {
+            const int i = idx / n, j = idx - i * n;
+            part += (long long)As[i * ld + j] * (long long)cs.Bp[i * ld + j];
+        }
+        for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        long long* red = reinterpret_cast<long long*>(cs.slots);  // slots are free until the first window
+        if ((t & 31) == 0) red[t >> 5] = part;
+        group_sync(bar, NT);
+        ChainScalars io{0, 0, kDigestSeed};
+        if (t == 0) {
+            long long c = 0;
+            for (int w = 0; w < NT / 32; ++w) c += red[w];
+            io.cost = io.best = c;
+        }
+        group_sync(bar, NT);
+        const NearSink sink{nullptr, nullptr, nullptr, 0};
+        const uint64_t acc = chain_run<TA, TB, NT>(As, cs, n, ld, M, 0ull, a.iters, a.sch, a.seed,
+                                                   a.chain_begin + (unsigned)ci, bar, t, a.wmax, io,
+                                                   sink);
+        for (int i = t; i < n; i += NT) a.best_perms[(size_t)ci * n + i] = cs.best_p[i];
+        if (t == 0) {
+            ChainResult r;
+            r.cost = io.cost;
+            r.best_cost = io.best;
+            r.accepted = acc;
+            r.near_ties = (unsigned long long)cs.flags[1];
+            r.digest = io.digest;
+            r.iterations = a.iters;
+            a.res[ci] = r;
+        }
+        group_sync(bar, NT);
+    }
+}
+
+// argmin over chains of (best_cost, chain id) and summed statistics; 1 CTA.
+__global__ void k_ens_reduce(const ChainResult* __restrict__ res, int count, long long* out /* 8 */) {
+    __shared__ long long sbest[32];
+    __shared__ int sidx[32];
+    __shared__ unsigned long long sacc[32], snear[32], sdig[32];
+    long long best = LLONG_MAX;
+    int bi = INT_MAX;
+    unsigned long long acc = 0, nr = 0, dg = 0;
+    for (int i = threadIdx.x; i < count; i += blockDim.x) {
+        const ChainResult r = res[i];
+        if (r.best_cost < best || (r.best_cost == best && i < bi)) { best = r.best_cost; bi = i; }
+        acc += r.accepted;
+        nr += r.near_ties;
+        dg ^= r.digest;
+    }
+    for (int o = 16; o; o >>= 1) {
+        const long long ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob < best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+        acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        nr += __shfl_xor_sync(0xffffffffu, nr, o);
+        dg ^= __shfl_xor_sync(0xffffffffu, dg, o);
+    }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) { sbest[w] = best; sidx[w] = bi; sacc[w] = acc; snear[w] = nr; sdig[w] = dg; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < (int)(blockDim.x >> 5); ++i) {
+            if (sbest[i] < best || (sbest[i] == best && sidx[i] < bi)) { best = sbest[i]; bi = sidx[i]; }
+            acc += sacc[i];
+            nr += snear[i];
+            dg ^= sdig[i];
+        }
+        out[0] = best;
+        out[1] = bi;
+        out[2] = (long long)acc;
+        out[3] = (long long)nr;
+        out[4] = (long long)dg;
+        out[5] = bi < count ? res[bi].cost : 0;
+    }
+}
+
+}  // namespace qapsa

@@ -1,0 +1,584 @@
+// qapsa.cu -- C ABI (include/qapsa.h): validation, device memory, launches.
+//
+// Every step of the hot path runs in the kernels of kernels.cuh; this file
+// only validates arguments, converts the int32 host matrices to their compact
+// device form (uint8 or uint16, rows padded to a multiple of 4 elements),
+// chooses the kernel instance and moves results back.  There is no CPU
+// fallback: without an sm_100 device the calls fail with QAP_E_CUDA.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/qapsa.h"
+#include "kernels.cuh"
+
+using namespace qapsa;
+
+struct qap_ctx {
+    int n = 0, ld = 0, M = 0, dev = 0;
+    cudaStream_t stream = nullptr;
+    int ta = 1, tb = 1;                 // bytes per A / B element on the device
+    void* dA = nullptr;
+    void* dB = nullptr;
+    int32_t *dp0 = nullptr, *dp = nullptr, *dbest = nullptr, *dD = nullptr, *dperm = nullptr;
+    DevState* dst = nullptr;
+    unsigned int* dnear_count = nullptr;
+    unsigned long long* dnear_k = nullptr;
+    unsigned char* dnear_dec = nullptr;
+    long long* dscratch = nullptr;      // 8 x int64
+    // ensemble buffers (grown on demand)
+    int32_t* ens_p0 = nullptr;
+    ChainResult* ens_res = nullptr;
+    uint16_t* ens_best = nullptr;
+    unsigned int* ens_counter = nullptr;
+    size_t ens_cap = 0;
+    bool delta_valid = false;
+    bool sticky = false;
+    std::string err;
+    int wmax = 1024, threads = 1024, force_global = 0, ens_group = 128;
+    int smem_optin = 0, num_sms = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    float last_ms = 0.f;
+    int last_launches = 0;
+};
+
+static thread_local std::string g_static_err;
+
+static qap_status fail(qap_ctx* c, qap_status st, const std::string& msg) {
+    if (c) c->err = msg;
+    else g_static_err = msg;
+    return st;
+}
+
+#define CU(call)                                                                             \
+    do {                                                                                     \
+        cudaError_t e_ = (call);                                                             \
+        if (e_ != cudaSuccess) {                                                             \
+            if (c) c->sticky = true;                                                         \
+            return fail(c, QAP_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+        }                                                                                    \
+    } while (0)
+
+#define CHECK_CTX(c)                                                        \
+    do {                                                                    \
+        if (!(c)) return fail(nullptr, QAP_E_INVALID_ARG, "ctx is NULL");  \
+        if ((c)->sticky) return QAP_E_CUDA;                                 \
+    } while (0)
+
+static bool is_perm(int n, const int32_t* p) {
+    std::vector<char> seen(n, 0);
+    for (int i = 0; i < n; ++i) {
+        if (p[i] < 0 || p[i] >= n || seen[p[i]]) return false;
+        seen[p[i]] = 1;
+    }
+    return true;
+}
+
+// A or B: symmetric, zero diagonal, 0 <= x <= 65535 (R12).
+static bool instance_ok(int n, const int32_t* X, int32_t* maxv, std::string* why, const char* name) {
+    int32_t mx = 0;
+    for (int i = 0; i < n; ++i) {
+        if (X[(size_t)i * n + i] != 0) { *why = std::string(name) + " has a nonzero diagonal"; return false; }
+        for (int j = 0; j < n; ++j) {
+            const int32_t v = X[(size_t)i * n + j];
+            if (v < 0 || v > 65535) { *why = std::string(name) + " entry outside [0, 65535]"; return false; }
+            if (v != X[(size_t)j * n + i]) { *why = std::string(name) + " is not symmetric"; return false; }
+            if (v > mx) mx = v;
+        }
+    }
+    *maxv = mx;
+    return true;
+}
+
+template <typename T>
+static std::vector<unsigned char> compact(int n, int ld, const int32_t* X) {
+    std::vector<unsigned char> out((size_t)n * ld * sizeof(T), 0);
+    T* o = reinterpret_cast<T*>(out.data());
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) o[(size_t)i * ld + j] = (T)X[(size_t)i * n + j];
+    return out;
+}
+
+static int chain_smem_bytes(const qap_ctx* c, int threads, bool d_smem) {
+    const GroupLayout L = group_layout(c->n, c->ld, c->M, c->tb, threads / 32, d_smem);
+    return align16(c->n * c->ld * c->ta) + L.bytes;
+}
+
+static qap_status validate_schedule(qap_ctx* c, const qap_schedule* s, uint64_t k0, uint64_t iters,
+                                    Sched* out) {
+    if (!s) return fail(c, QAP_E_INVALID_ARG, "schedule is NULL");
+    if (s->kind != QAP_COOL_GEOMETRIC && s->kind != QAP_COOL_LUNDY_MEES)
+        return fail(c, QAP_E_SCHEDULE, "unknown cooling kind");
+    if (s->reserved != 0) return fail(c, QAP_E_SCHEDULE, "reserved field must be 0");
+    if (!std::isfinite(s->t0) || !std::isfinite(s->tf) || !(s->tf > 0.0) || !(s->t0 >= s->tf))
+        return fail(c, QAP_E_SCHEDULE, "need finite t0 >= tf > 0");
+    if (s->total_iters == 0) return fail(c, QAP_E_SCHEDULE, "total_iters == 0");
+    if (k0 > s->total_iters || iters > s->total_iters - k0)
+        return fail(c, QAP_E_SCHEDULE, "iteration range exceeds total_iters");
+    // R1: coefficients once on the host, in double.
+    const double I1 = (double)(s->total_iters - 1);
+    out->kind = s->kind;
+    out->t0 = s->t0;
+    if (s->kind == QAP_COOL_GEOMETRIC)
+        out->coef = s->total_iters > 1 ? std::log(s->tf / s->t0) / I1 : 0.0;
+    else
+        out->coef = s->total_iters > 1 ? (s->t0 - s->tf) / ((I1 * s->t0) * s->tf) : 0.0;
+    return QAP_OK;
+}
+
+extern "C" {
+
+int32_t qap_version(void) { return QAPSA_VERSION; }
+
+const char* qap_status_str(qap_status st) {
+    switch (st) {
+        case QAP_OK: return "QAP_OK";
+        case QAP_E_INVALID_ARG: return "QAP_E_INVALID_ARG";
+        case QAP_E_DIMENSION: return "QAP_E_DIMENSION";
+        case QAP_E_UNSUPPORTED: return "QAP_E_UNSUPPORTED";
+        case QAP_E_OVERFLOW: return "QAP_E_OVERFLOW";
+        case QAP_E_SCHEDULE: return "QAP_E_SCHEDULE";
+        case QAP_E_STATE: return "QAP_E_STATE";
+        case QAP_E_CUDA: return "QAP_E_CUDA";
+        case QAP_E_NOMEM: return "QAP_E_NOMEM";
+    }
+    return "QAP_E_UNKNOWN";
+}
+
+const char* qap_last_error(const qap_ctx* ctx) {
+    return ctx ? ctx->err.c_str() : g_static_err.c_str();
+}
+
+void qap_destroy(qap_ctx* c) {
+    if (!c) return;
+    void* ptrs[] = {c->dA, c->dB, c->dp0, c->dp, c->dbest, c->dD, c->dperm, c->dst, c->dnear_count,
+                    c->dnear_k, c->dnear_dec, c->dscratch, c->ens_p0, c->ens_res, c->ens_best,
+                    c->ens_counter};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    if (c->ev0) cudaEventDestroy(c->ev0);
+    if (c->ev1) cudaEventDestroy(c->ev1);
+    delete c;
+}
+
+static qap_status launch_reset(qap_ctx* c, const int32_t* src) {
+    if (c->ta == 1 && c->tb == 1)
+        k_reset<uint8_t, uint8_t><<<1, 512, 0, c->stream>>>((const uint8_t*)c->dA, (const uint8_t*)c->dB, src, c->n, c->ld, c->dp, c->dbest, c->dst);
+    else if (c->ta == 1)
+        k_reset<uint8_t, uint16_t><<<1, 512, 0, c->stream>>>((const uint8_t*)c->dA, (const uint16_t*)c->dB, src, c->n, c->ld, c->dp, c->dbest, c->dst);
+    else if (c->tb == 1)
+        k_reset<uint16_t, uint8_t><<<1, 512, 0, c->stream>>>((const uint16_t*)c->dA, (const uint8_t*)c->dB, src, c->n, c->ld, c->dp, c->dbest, c->dst);
+    else
+        k_reset<uint16_t, uint16_t><<<1, 512, 0, c->stream>>>((const uint16_t*)c->dA, (const uint16_t*)c->dB, src, c->n, c->ld, c->dp, c->dbest, c->dst);
+    CU(cudaGetLastError());
+    CU(cudaMemsetAsync(c->dnear_count, 0, sizeof(unsigned int), c->stream));
+    c->delta_valid = false;
+    return QAP_OK;
+}
+
+qap_status qap_create(int32_t n, const int32_t* A, const int32_t* B, const int32_t* p0, int32_t device,
+                      void* stream, qap_ctx** out) {
+    qap_ctx* c = nullptr;
+    if (!out || !A || !B || !p0) return fail(nullptr, QAP_E_INVALID_ARG, "NULL argument");
+    *out = nullptr;
+    if (n < 2 || n > QAP_MAX_N) return fail(nullptr, QAP_E_INVALID_ARG, "n out of range");
+    std::string why;
+    int32_t maxA = 0, maxB = 0;
+    if (!instance_ok(n, A, &maxA, &why, "A") || !instance_ok(n, B, &maxB, &why, "B"))
+        return fail(nullptr, QAP_E_UNSUPPORTED, why);
+    // R13: every partial dot product and Δ entry stays below 2^31.
+    if (4.0 * (double)n * (double)maxA * (double)maxB >= 2147483648.0)
+        return fail(nullptr, QAP_E_OVERFLOW, "4 n maxA maxB >= 2^31");
+    if (!is_perm(n, p0)) return fail(nullptr, QAP_E_DIMENSION, "p0 is not a permutation");
+
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(nullptr, QAP_E_CUDA, "no CUDA device (libqapsa has no CPU fallback)");
+    if (device < 0 || device >= ndev) return fail(nullptr, QAP_E_INVALID_ARG, "bad device ordinal");
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major < 10)
+        return fail(nullptr, QAP_E_CUDA, "device is not sm_100 (Blackwell)");
+
+    c = new qap_ctx();
+    c->n = n;
+    c->ld = (n + 3) & ~3;
+    c->M = n * (n - 1) / 2;
+    c->dev = device;
+    c->stream = (cudaStream_t)stream;
+    c->ta = maxA <= 255 ? 1 : 2;
+    c->tb = maxB <= 255 ? 1 : 2;
+    c->smem_optin = (int)prop.sharedMemPerBlockOptin;
+    c->num_sms = prop.multiProcessorCount;
+    if (cudaSetDevice(device) != cudaSuccess) {
+        delete c;
+        return fail(nullptr, QAP_E_CUDA, "cudaSetDevice failed");
+    }
+    // A and B' must fit on one SM (Δ may spill to global memory / L2).
+    if (chain_smem_bytes(c, 256, false) > c->smem_optin) {
+        delete c;
+        return fail(nullptr, QAP_E_UNSUPPORTED, "A and B' do not fit in one SM's shared memory");
+    }
+    const size_t nA = (size_t)n * c->ld * c->ta, nB = (size_t)n * c->ld * c->tb;
+    auto hA = c->ta == 1 ? compact<uint8_t>(n, c->ld, A) : compact<uint16_t>(n, c->ld, A);
+    auto hB = c->tb == 1 ? compact<uint8_t>(n, c->ld, B) : compact<uint16_t>(n, c->ld, B);
+    qap_status st = QAP_OK;
+    auto alloc = [&](void** p, size_t bytes) {
+        if (st != QAP_OK) return;
+        if (cudaMalloc(p, bytes) != cudaSuccess) st = fail(nullptr, QAP_E_NOMEM, "cudaMalloc failed");
+    };
+    alloc(&c->dA, nA);
+    alloc(&c->dB, nB);
+    alloc((void**)&c->dp0, n * 4);
+    alloc((void**)&c->dp, n * 4);
+    alloc((void**)&c->dbest, n * 4);
+    alloc((void**)&c->dperm, n * 4);
+    alloc((void**)&c->dD, (size_t)(c->M + 4) * 4);
+    alloc((void**)&c->dst, sizeof(DevState));
+    alloc((void**)&c->dnear_count, sizeof(unsigned int));
+    alloc((void**)&c->dnear_k, QAP_NEAR_LOG_CAP * sizeof(unsigned long long));
+    alloc((void**)&c->dnear_dec, QAP_NEAR_LOG_CAP);
+    alloc((void**)&c->dscratch, 8 * sizeof(long long));
+    if (st != QAP_OK) {
+        qap_destroy(c);
+        return st;
+    }
+    if (cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess) {
+        qap_destroy(c);
+        return fail(nullptr, QAP_E_CUDA, "cudaEventCreate failed");
+    }
+    cudaError_t e = cudaMemcpyAsync(c->dA, hA.data(), nA, cudaMemcpyHostToDevice, c->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(c->dB, hB.data(), nB, cudaMemcpyHostToDevice, c->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(c->dp0, p0, n * 4, cudaMemcpyHostToDevice, c->stream);
+    if (e != cudaSuccess) {
+        std::string m = cudaGetErrorString(e);
+        qap_destroy(c);
+        return fail(nullptr, QAP_E_CUDA, m);
+    }
+    st = launch_reset(c, c->dp0);
+    if (st == QAP_OK && cudaStreamSynchronize(c->stream) != cudaSuccess)
+        st = fail(c, QAP_E_CUDA, "create: stream synchronize failed");
+    if (st != QAP_OK) {
+        g_static_err = c->err;
+        qap_destroy(c);
+        return st;
+    }
+    c->last_launches = 1;
+    *out = c;
+    return QAP_OK;
+}
+
+qap_status qap_reset(qap_ctx* c, const int32_t* perm) {
+    CHECK_CTX(c);
+    if (perm && !is_perm(c->n, perm)) return fail(c, QAP_E_DIMENSION, "perm is not a permutation");
+    CU(cudaSetDevice(c->dev));
+    const int32_t* src = c->dp0;
+    if (perm) {
+        CU(cudaMemcpyAsync(c->dperm, perm, c->n * 4, cudaMemcpyHostToDevice, c->stream));
+        src = c->dperm;
+    }
+    qap_status st = launch_reset(c, src);
+    if (st != QAP_OK) return st;
+    CU(cudaStreamSynchronize(c->stream));
+    c->last_launches = 1;
+    return QAP_OK;
+}
+
+qap_status qap_delta_init(qap_ctx* c) {
+    CHECK_CTX(c);
+    CU(cudaSetDevice(c->dev));
+    const int threads = 256, blocks = (c->M + threads - 1) / threads;
+    if (c->ta == 1 && c->tb == 1)
+        k_delta_init<uint8_t, uint8_t><<<blocks, threads, 0, c->stream>>>((const uint8_t*)c->dA, (const uint8_t*)c->dB, c->dp, c->n, c->ld, c->M, c->dD);
+    else if (c->ta == 1)
+        k_delta_init<uint8_t, uint16_t><<<blocks, threads, 0, c->stream>>>((const uint8_t*)c->dA, (const uint16_t*)c->dB, c->dp, c->n, c->ld, c->M, c->dD);
+    else if (c->tb == 1)
+        k_delta_init<uint16_t, uint8_t><<<blocks, threads, 0, c->stream>>>((const uint16_t*)c->dA, (const uint8_t*)c->dB, c->dp, c->n, c->ld, c->M, c->dD);
+    else
+        k_delta_init<uint16_t, uint16_t><<<blocks, threads, 0, c->stream>>>((const uint16_t*)c->dA, (const uint16_t*)c->dB, c->dp, c->n, c->ld, c->M, c->dD);
+    CU(cudaGetLastError());
+    CU(cudaStreamSynchronize(c->stream));
+    c->delta_valid = true;
+    c->last_launches = 1;
+    return QAP_OK;
+}
+
+}  // extern "C"
+
+template <typename TA, typename TB, int NT, bool DS>
+static cudaError_t launch_chain_t(qap_ctx* c, const ChainArgs& a, int smem) {
+    auto kern = k_sa_chain<TA, TB, NT, DS>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    kern<<<1, NT, smem, c->stream>>>(a);
+    return cudaGetLastError();
+}
+
+template <typename TA, typename TB>
+static cudaError_t launch_chain_tt(qap_ctx* c, const ChainArgs& a, int threads, bool ds, int smem) {
+    if (threads == 1024) return ds ? launch_chain_t<TA, TB, 1024, true>(c, a, smem) : launch_chain_t<TA, TB, 1024, false>(c, a, smem);
+    if (threads == 512) return ds ? launch_chain_t<TA, TB, 512, true>(c, a, smem) : launch_chain_t<TA, TB, 512, false>(c, a, smem);
+    return ds ? launch_chain_t<TA, TB, 256, true>(c, a, smem) : launch_chain_t<TA, TB, 256, false>(c, a, smem);
+}
+
+extern "C" {
+
+qap_status qap_sa_run(qap_ctx* c, uint64_t k0, uint64_t iters, const qap_schedule* s, uint64_t seed,
+                      qap_stats* out) {
+    CHECK_CTX(c);
+    if (iters == 0) return fail(c, QAP_E_INVALID_ARG, "iters == 0");
+    Sched sch;
+    qap_status vs = validate_schedule(c, s, k0, iters, &sch);
+    if (vs != QAP_OK) return vs;
+    if (!c->delta_valid) return fail(c, QAP_E_STATE, "Δ not initialised: call qap_delta_init");
+    CU(cudaSetDevice(c->dev));
+    DevState before;
+    unsigned int near_before = 0;
+    CU(cudaMemcpyAsync(&before, c->dst, sizeof before, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaMemcpyAsync(&near_before, c->dnear_count, sizeof near_before, cudaMemcpyDeviceToHost, c->stream));
+
+    int threads = c->threads;
+    bool ds = !c->force_global && chain_smem_bytes(c, threads, true) <= c->smem_optin;
+    const int smem = chain_smem_bytes(c, threads, ds);
+    if (smem > c->smem_optin) return fail(c, QAP_E_UNSUPPORTED, "chain state does not fit on chip");
+
+    ChainArgs a;
+    a.A = c->dA; a.B = c->dB; a.p = c->dp; a.best_p = c->dbest; a.D = c->dD; a.st = c->dst;
+    a.near_count = c->dnear_count; a.near_k = c->dnear_k; a.near_dec = c->dnear_dec;
+    a.near_cap = QAP_NEAR_LOG_CAP;
+    a.n = c->n; a.ld = c->ld; a.M = c->M; a.wmax = std::min(c->wmax, threads);
+    a.k0 = k0; a.k_end = k0 + iters; a.seed = seed; a.sch = sch;
+
+    CU(cudaEventRecord(c->ev0, c->stream));
+    cudaError_t e;
+    if (c->ta == 1 && c->tb == 1) e = launch_chain_tt<uint8_t, uint8_t>(c, a, threads, ds, smem);
+    else if (c->ta == 1) e = launch_chain_tt<uint8_t, uint16_t>(c, a, threads, ds, smem);
+    else if (c->tb == 1) e = launch_chain_tt<uint16_t, uint8_t>(c, a, threads, ds, smem);
+    else e = launch_chain_tt<uint16_t, uint16_t>(c, a, threads, ds, smem);
+    CU(e);
+    CU(cudaEventRecord(c->ev1, c->stream));
+    DevState after;
+    unsigned int near_after = 0;
+    CU(cudaMemcpyAsync(&after, c->dst, sizeof after, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaMemcpyAsync(&near_after, c->dnear_count, sizeof near_after, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    CU(cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1));
+    c->last_launches = 1;
+    if (out) {
+        out->iterations = iters;
+        out->accepted = after.accepted - before.accepted;
+        out->near_ties = near_after - near_before;
+        out->cost = after.cost;
+        out->best_cost = after.best_cost;
+        out->digest = after.digest;
+    }
+    return QAP_OK;
+}
+
+qap_status qap_cost(qap_ctx* c, const int32_t* perm, int64_t* out) {
+    CHECK_CTX(c);
+    if (!out) return fail(c, QAP_E_INVALID_ARG, "out is NULL");
+    if (perm && !is_perm(c->n, perm)) return fail(c, QAP_E_DIMENSION, "perm is not a permutation");
+    CU(cudaSetDevice(c->dev));
+    const int32_t* src = c->dp;
+    if (perm) {
+        CU(cudaMemcpyAsync(c->dperm, perm, c->n * 4, cudaMemcpyHostToDevice, c->stream));
+        src = c->dperm;
+    }
+    if (c->ta == 1 && c->tb == 1)
+        k_cost<uint8_t, uint8_t><<<1, 512, 0, c->stream>>>((const uint8_t*)c->dA, (const uint8_t*)c->dB, src, c->n, c->ld, c->dscratch);
+    else if (c->ta == 1)
+        k_cost<uint8_t, uint16_t><<<1, 512, 0, c->stream>>>((const uint8_t*)c->dA, (const uint16_t*)c->dB, src, c->n, c->ld, c->dscratch);
+    else if (c->tb == 1)
+        k_cost<uint16_t, uint8_t><<<1, 512, 0, c->stream>>>((const uint16_t*)c->dA, (const uint8_t*)c->dB, src, c->n, c->ld, c->dscratch);
+    else
+        k_cost<uint16_t, uint16_t><<<1, 512, 0, c->stream>>>((const uint16_t*)c->dA, (const uint16_t*)c->dB, src, c->n, c->ld, c->dscratch);
+    CU(cudaGetLastError());
+    long long v = 0;
+    CU(cudaMemcpyAsync(&v, c->dscratch, sizeof v, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    *out = v;
+    c->last_launches = 1;
+    return QAP_OK;
+}
+
+qap_status qap_get_state(qap_ctx* c, int32_t* perm, int32_t* best_perm, int32_t* delta) {
+    CHECK_CTX(c);
+    if (delta && !c->delta_valid) return fail(c, QAP_E_STATE, "Δ not initialised");
+    CU(cudaSetDevice(c->dev));
+    if (perm) CU(cudaMemcpyAsync(perm, c->dp, c->n * 4, cudaMemcpyDeviceToHost, c->stream));
+    if (best_perm) CU(cudaMemcpyAsync(best_perm, c->dbest, c->n * 4, cudaMemcpyDeviceToHost, c->stream));
+    if (delta) CU(cudaMemcpyAsync(delta, c->dD, (size_t)c->M * 4, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    c->last_launches = 0;
+    return QAP_OK;
+}
+
+qap_status qap_get_near_ties(qap_ctx* c, uint64_t* ks, uint8_t* decisions, int32_t cap, int32_t* count) {
+    CHECK_CTX(c);
+    if (cap < 0 || !count || (cap > 0 && (!ks || !decisions)))
+        return fail(c, QAP_E_INVALID_ARG, "bad near-tie buffers");
+    CU(cudaSetDevice(c->dev));
+    unsigned int cnt = 0;
+    CU(cudaMemcpyAsync(&cnt, c->dnear_count, sizeof cnt, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    int m = std::min<int>(std::min<unsigned>(cnt, QAP_NEAR_LOG_CAP), cap);
+    if (m > 0) {
+        CU(cudaMemcpyAsync(ks, c->dnear_k, m * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
+        CU(cudaMemcpyAsync(decisions, c->dnear_dec, m, cudaMemcpyDeviceToHost, c->stream));
+        CU(cudaStreamSynchronize(c->stream));
+    }
+    *count = (int32_t)cnt;
+    return QAP_OK;
+}
+
+qap_status qap_schedule_bounds(qap_ctx* c, double* t0, double* tf) {
+    CHECK_CTX(c);
+    if (!t0 || !tf) return fail(c, QAP_E_INVALID_ARG, "NULL output");
+    if (!c->delta_valid) return fail(c, QAP_E_STATE, "Δ not initialised");
+    CU(cudaSetDevice(c->dev));
+    k_delta_bounds<<<1, 1024, 0, c->stream>>>(c->dD, c->M, reinterpret_cast<int*>(c->dscratch));
+    CU(cudaGetLastError());
+    int mm[2];
+    CU(cudaMemcpyAsync(mm, c->dscratch, sizeof mm, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    if (mm[1] == 0) {
+        *t0 = 1.0;
+        *tf = 0.1;
+    } else {  // R2
+        *t0 = (double)mm[0] + ((double)mm[1] - (double)mm[0]) / 10.0;
+        *tf = (double)mm[0];
+    }
+    c->last_launches = 1;
+    return QAP_OK;
+}
+
+}  // extern "C"
+
+template <typename TA, typename TB, int NT>
+static cudaError_t launch_ens_t(qap_ctx* c, const EnsArgs& a, int groups, int smem) {
+    auto kern = k_ensemble<TA, TB, NT>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    const int blocks = std::min(c->num_sms, (a.count + groups - 1) / groups);
+    kern<<<blocks, NT * groups, smem, c->stream>>>(a);
+    return cudaGetLastError();
+}
+
+template <typename TA, typename TB>
+static cudaError_t launch_ens_tt(qap_ctx* c, const EnsArgs& a, int nt, int groups, int smem) {
+    if (nt == 256) return launch_ens_t<TA, TB, 256>(c, a, groups, smem);
+    if (nt == 64) return launch_ens_t<TA, TB, 64>(c, a, groups, smem);
+    return launch_ens_t<TA, TB, 128>(c, a, groups, smem);
+}
+
+extern "C" {
+
+qap_status qap_ensemble_run(qap_ctx* c, uint32_t chain_begin, uint32_t chain_count, const int32_t* p0s,
+                            uint64_t iters, const qap_schedule* s, uint64_t seed, int64_t* best_cost,
+                            uint32_t* best_chain, int32_t* best_perm, qap_stats* sum_stats,
+                            qap_chain_result* per_chain) {
+    CHECK_CTX(c);
+    if (!p0s || !best_cost || !best_chain || !best_perm) return fail(c, QAP_E_INVALID_ARG, "NULL argument");
+    if (chain_count == 0 || iters == 0) return fail(c, QAP_E_INVALID_ARG, "chain_count or iters is 0");
+    Sched sch;
+    qap_status vs = validate_schedule(c, s, 0, iters, &sch);
+    if (vs != QAP_OK) return vs;
+    const int n = c->n;
+    for (uint32_t i = 0; i < chain_count; ++i)
+        if (!is_perm(n, p0s + (size_t)i * n)) return fail(c, QAP_E_DIMENSION, "a start permutation is invalid");
+    const int nt = c->ens_group;
+    const GroupLayout L = group_layout(n, c->ld, c->M, c->tb, nt / 32, true);
+    const int a_bytes = align16(n * c->ld * c->ta);
+    int groups = std::min((c->smem_optin - a_bytes) / L.bytes, 1024 / nt);
+    if (groups < 1) return fail(c, QAP_E_UNSUPPORTED, "one ensemble chain does not fit on chip");
+    const int smem = a_bytes + groups * L.bytes;
+    CU(cudaSetDevice(c->dev));
+    if (c->ens_cap < chain_count) {
+        if (c->ens_p0) cudaFree(c->ens_p0);
+        if (c->ens_res) cudaFree(c->ens_res);
+        if (c->ens_best) cudaFree(c->ens_best);
+        c->ens_p0 = nullptr; c->ens_res = nullptr; c->ens_best = nullptr; c->ens_cap = 0;
+        if (cudaMalloc(&c->ens_p0, (size_t)chain_count * n * 4) != cudaSuccess ||
+            cudaMalloc(&c->ens_res, (size_t)chain_count * sizeof(ChainResult)) != cudaSuccess ||
+            cudaMalloc(&c->ens_best, (size_t)chain_count * n * 2) != cudaSuccess)
+            return fail(c, QAP_E_NOMEM, "ensemble buffers");
+        c->ens_cap = chain_count;
+    }
+    if (!c->ens_counter) CU(cudaMalloc(&c->ens_counter, sizeof(unsigned int)));
+    CU(cudaMemcpyAsync(c->ens_p0, p0s, (size_t)chain_count * n * 4, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemsetAsync(c->ens_counter, 0, sizeof(unsigned int), c->stream));
+    EnsArgs a;
+    a.A = c->dA; a.B = c->dB; a.p0s = c->ens_p0; a.res = c->ens_res; a.best_perms = c->ens_best;
+    a.next_chain = c->ens_counter; a.count = (int)chain_count; a.n = n; a.ld = c->ld; a.M = c->M;
+    a.wmax = std::min(c->wmax, nt); a.chain_begin = chain_begin; a.iters = iters; a.seed = seed; a.sch = sch;
+    CU(cudaEventRecord(c->ev0, c->stream));
+    cudaError_t e;
+    if (c->ta == 1 && c->tb == 1) e = launch_ens_tt<uint8_t, uint8_t>(c, a, nt, groups, smem);
+    else if (c->ta == 1) e = launch_ens_tt<uint8_t, uint16_t>(c, a, nt, groups, smem);
+    else if (c->tb == 1) e = launch_ens_tt<uint16_t, uint8_t>(c, a, nt, groups, smem);
+    else e = launch_ens_tt<uint16_t, uint16_t>(c, a, nt, groups, smem);
+    CU(e);
+    CU(cudaEventRecord(c->ev1, c->stream));
+    k_ens_reduce<<<1, 1024, 0, c->stream>>>(c->ens_res, (int)chain_count, c->dscratch);
+    CU(cudaGetLastError());
+    long long red[8];
+    CU(cudaMemcpyAsync(red, c->dscratch, sizeof red, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    const int bi = (int)red[1];
+    std::vector<uint16_t> bp(n);
+    CU(cudaMemcpy(bp.data(), c->ens_best + (size_t)bi * n, n * 2, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < n; ++i) best_perm[i] = bp[i];
+    *best_cost = red[0];
+    *best_chain = chain_begin + (uint32_t)bi;
+    if (sum_stats) {
+        sum_stats->iterations = iters * (uint64_t)chain_count;
+        sum_stats->accepted = (uint64_t)red[2];
+        sum_stats->near_ties = (uint64_t)red[3];
+        sum_stats->digest = (uint64_t)red[4];
+        sum_stats->cost = red[5];
+        sum_stats->best_cost = red[0];
+    }
+    if (per_chain) {
+        static_assert(sizeof(ChainResult) == sizeof(qap_chain_result), "layout");
+        CU(cudaMemcpy(per_chain, c->ens_res, (size_t)chain_count * sizeof(ChainResult), cudaMemcpyDeviceToHost));
+    }
+    CU(cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1));
+    c->last_launches = 2;
+    return QAP_OK;
+}
+
+qap_status qap_set_option(qap_ctx* c, int32_t key, int64_t value) {
+    CHECK_CTX(c);
+    switch (key) {
+        case QAP_OPT_WINDOW_MAX:
+            if (value < 32 || value > 1024 || (value & 31)) return fail(c, QAP_E_INVALID_ARG, "window must be a multiple of 32 in [32,1024]");
+            c->wmax = (int)value;
+            return QAP_OK;
+        case QAP_OPT_THREADS:
+            if (value != 256 && value != 512 && value != 1024) return fail(c, QAP_E_INVALID_ARG, "threads must be 256, 512 or 1024");
+            c->threads = (int)value;
+            return QAP_OK;
+        case QAP_OPT_FORCE_GLOBAL_DELTA:
+            c->force_global = value ? 1 : 0;
+            return QAP_OK;
+        case QAP_OPT_ENSEMBLE_GROUP:
+            if (value != 64 && value != 128 && value != 256) return fail(c, QAP_E_INVALID_ARG, "group must be 64, 128 or 256");
+            c->ens_group = (int)value;
+            return QAP_OK;
+    }
+    return fail(c, QAP_E_INVALID_ARG, "unknown option");
+}
+
+qap_status qap_last_kernel_time(qap_ctx* c, float* ms, int32_t* launches) {
+    CHECK_CTX(c);
+    if (ms) *ms = c->last_ms;
+    if (launches) *launches = c->last_launches;
+    return QAP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,271 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs.  Integers (Δ, p, C, counters, digest) must be bit-exact;
+Eq.(2) decisions may differ only at flagged near ties (R16), which the oracle
+then follows.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_1208_2675_b200 import qapsa as Q
+from qap_inputs import SA_SEED, config, grey_density, start_perm, start_perms, taixxa
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+
+def _sched(s: O.Schedule):
+    return Q.make_schedule(s.kind, s.t0, s.tf, s.total_iters)
+
+
+def _compare_run(A, B, p0, I, sched: O.Schedule, seed=SA_SEED, opts=(), k_splits=None,
+                 mode=O.MODE_DELTA):
+    """GPU run of iterations [0, I) vs the oracle; returns the GPU stats."""
+    with Q.Solver(A, B, p0) as s:
+        for k, v in opts:
+            s.set_option(k, v)
+        s.delta_init()
+        bounds = k_splits or [0, I]
+        tot_acc = 0
+        for a, b in zip(bounds, bounds[1:]):
+            g = s.run(a, b - a, _sched(sched), seed)
+            tot_acc += g["accepted"]
+        p, bp, D = s.state()
+        n_near, near = s.near_ties()
+        gcost = s.cost()
+    ref = O.Run(A, B, p0, mode=mode)
+    o = ref.run(0, I, sched, seed, follow=near)
+    assert n_near == o["near_ties"]
+    assert tot_acc == o["accepted"]
+    for key in ("cost", "best_cost", "digest"):
+        assert g[key] == o[key], key
+    np.testing.assert_array_equal(p, ref.p)
+    np.testing.assert_array_equal(bp, ref.best_p)
+    assert gcost == O.cost(A, B, p) == o["cost"]
+    if mode == O.MODE_DELTA:
+        np.testing.assert_array_equal(D.astype(np.int64), ref.D)
+    else:
+        np.testing.assert_array_equal(D.astype(np.int64), O.delta_init(A, O.bprime(B, p)))
+    return g, tot_acc
+
+
+# ---------------- a1: Δ-init, Eq.(1), schedule bounds ----------------
+
+@pytest.mark.parametrize("n,seed", [(2, 1), (3, 2), (5, 3), (12, 12), (33, 4), (50, 50), (64, 5),
+                                    (100, 100), (129, 6), (200, 7), (256, 8)])
+def test_delta_init_bit_exact(n, seed):
+    A, B = taixxa(n, seed)
+    p0 = start_perm(n, seed, 3)
+    with Q.Solver(A, B, p0) as s:
+        s.delta_init()
+        _, _, D = s.state()
+        assert s.cost() == O.cost(A, B, p0)
+        q = start_perm(n, seed, 4)
+        assert s.cost(q) == O.cost(A, B, q)
+        ref = O.delta_init(A, O.bprime(B, p0))
+        np.testing.assert_array_equal(D.astype(np.int64), ref)
+        t0, tf = s.schedule_bounds()
+        assert (t0, tf) == O.temperature_bounds(ref, n)
+
+
+def test_delta_init_uint16_grey_density():
+    A, B = grey_density(256)
+    p0 = start_perm(256, SA_SEED, 0)
+    with Q.Solver(A, B, p0) as s:
+        s.delta_init()
+        _, _, D = s.state()
+        np.testing.assert_array_equal(D.astype(np.int64), O.delta_init(A, O.bprime(B, p0)))
+        assert s.cost() == O.cost(A, B, p0)
+
+
+def test_reset_restores_p0_and_perm():
+    A, B = taixxa(20, 1)
+    p0 = start_perm(20, 1, 0)
+    with Q.Solver(A, B, p0) as s:
+        s.delta_init()
+        sch = O.geometric_schedule_for(A, B, p0, 5000)
+        s.run(0, 5000, _sched(sch), 1)
+        s.reset()
+        p, bp, _ = s.state(want_delta=False)
+        np.testing.assert_array_equal(p, p0)
+        np.testing.assert_array_equal(bp, p0)
+        with pytest.raises(Q.QapError):          # Δ invalid after reset
+            s.run(0, 10, _sched(sch), 1)
+        q = start_perm(20, 2, 0)
+        s.reset(q)
+        assert s.cost() == O.cost(A, B, q)
+
+
+# ---------------- a2-a7: full trajectories ----------------
+
+def test_config1_full_bit_exact():
+    A, B, p0, cfg = config(1)
+    sch = O.geometric_schedule_for(A, B, p0, cfg["iters"])
+    g, acc = _compare_run(A, B, p0, cfg["iters"], sch)
+    assert acc > 100
+
+
+def test_config2_full_bit_exact():
+    A, B, p0, cfg = config(2)
+    sch = O.geometric_schedule_for(A, B, p0, cfg["iters"])
+    _compare_run(A, B, p0, cfg["iters"], sch, mode=O.MODE_SCRATCH)
+
+
+@pytest.mark.parametrize("threads,wmax", [(256, 32), (512, 128), (1024, 1024), (1024, 64),
+                                          (256, 256)])
+def test_window_and_cta_shape_invariance(threads, wmax):
+    """result independent of window size and CTA shape."""
+    A, B = taixxa(50, 77)
+    p0 = start_perm(50, 5, 0)
+    sch = O.geometric_schedule_for(A, B, p0, 200000)
+    _compare_run(A, B, p0, 200000, sch, opts=[(Q.QAP_OPT_THREADS, threads),
+                                                (Q.QAP_OPT_WINDOW_MAX, wmax)])
+
+
+def test_resume_split_calls():
+    A, B = taixxa(37, 9)
+    p0 = start_perm(37, 9, 0)
+    I = 300000
+    sch = O.geometric_schedule_for(A, B, p0, I)
+    _compare_run(A, B, p0, I, sch, k_splits=[0, 1, 999, 1000, 123457, I])
+
+
+def test_global_delta_variant():
+    """Δ kept in global memory / L2 (the spill path) gives the same trajectory."""
+    A, B = taixxa(64, 3)
+    p0 = start_perm(64, 3, 0)
+    sch = O.geometric_schedule_for(A, B, p0, 200000)
+    _compare_run(A, B, p0, 200000, sch, opts=[(Q.QAP_OPT_FORCE_GLOBAL_DELTA, 1)])
+
+
+def test_lundy_mees_schedule():
+    A, B = taixxa(30, 30)
+    p0 = start_perm(30, 1, 0)
+    g = O.geometric_schedule_for(A, B, p0, 100000)
+    sch = O.Schedule(O.COOL_LUNDY_MEES, g.t0, g.tf, 100000)
+    _compare_run(A, B, p0, 100000, sch)
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 5, 7])
+def test_tiny_instances_window_wraps(n):
+    """M < window: candidates wrap around the triangle many times per window."""
+    A, B = taixxa(n, 40 + n)
+    p0 = start_perm(n, n, 0)
+    sch = O.geometric_schedule_for(A, B, p0, 20000)
+    _compare_run(A, B, p0, 20000, sch)
+
+
+def test_all_zero_flow_every_iteration_accepts():
+    n = 16
+    _, B = taixxa(n, 2)
+    A = np.zeros((n, n), np.int32)
+    p0 = start_perm(n, 1, 0)
+    sch = O.Schedule(O.COOL_GEOMETRIC, 1.0, 0.1, 5000)
+    g, acc = _compare_run(A, B, p0, 5000, sch)
+    assert acc == 5000 and g["cost"] == 0
+
+
+def test_single_iteration_and_tail_of_schedule():
+    A, B = taixxa(25, 2)
+    p0 = start_perm(25, 2, 0)
+    sch = O.geometric_schedule_for(A, B, p0, 10**6)
+    with Q.Solver(A, B, p0) as s:
+        s.delta_init()
+        g = s.run(10**6 - 1, 1, _sched(sch), 7)
+        _, _, D = s.state()
+    ref = O.Run(A, B, p0)
+    o = ref.run(10**6 - 1, 1, sch, 7)
+    assert g["cost"] == o["cost"] and g["digest"] == o["digest"]
+    np.testing.assert_array_equal(D.astype(np.int64), ref.D)
+
+
+def test_schedule_errors():
+    A, B = taixxa(10, 1)
+    p0 = start_perm(10, 1, 0)
+    with Q.Solver(A, B, p0) as s:
+        with pytest.raises(Q.QapError) as e:
+            s.run(0, 10, Q.make_schedule(0, 1.0, 0.5, 100), 1)     # Δ not initialised
+        assert e.value.status == 6
+        s.delta_init()
+        for bad in [Q.make_schedule(0, 1.0, 2.0, 100), Q.make_schedule(0, 1.0, 0.0, 100),
+                    Q.make_schedule(5, 1.0, 0.5, 100), Q.make_schedule(0, 1.0, 0.5, 5)]:
+            with pytest.raises(Q.QapError) as e:
+                s.run(0, 10, bad, 1)
+            assert e.value.status == 5
+
+
+def test_grey_density_uint16_prefix():
+    """Config-4-shaped instance (uint16 B, δ≡0 plateau): first 3e5 iterations of
+    its 1e9-iteration schedule, Δ spilled to global memory."""
+    A, B = grey_density(256)
+    p0 = start_perm(256, SA_SEED, 0)
+    sch = O.geometric_schedule_for(A, B, p0, 10**9)
+    g, acc = _compare_run(A, B, p0, 300000, sch, mode=O.MODE_SCRATCH)
+    assert acc > 100000
+
+
+# ---------------- a8: ensemble ----------------
+
+def test_ensemble_per_chain_bit_exact():
+    A, B = taixxa(40, 40)
+    p0s = start_perms(40, SA_SEED, 100, 50)
+    sch = O.geometric_schedule_for(A, B, p0s[0], 30000)
+    with Q.Solver(A, B, p0s[0]) as s:
+        res = s.ensemble(100, p0s, 30000, _sched(sch), SA_SEED, per_chain=True)
+    ref = O.ensemble_run(A, B, p0s, 100, 30000, sch, SA_SEED)
+    for i, r in enumerate(res["per_chain"]):
+        if r["near_ties"]:
+            continue
+        assert (r["cost"], r["best_cost"], r["accepted"], r["iterations"]) == tuple(
+            int(x) for x in ref[i, [0, 1, 2, 5]])
+        assert np.uint64(r["digest"]) == np.int64(ref[i, 4]).astype(np.uint64)
+    bi = int(np.lexsort((np.arange(50), ref[:, 1]))[0])
+    assert res["best_chain"] == 100 + bi and res["best_cost"] == ref[bi, 1]
+    assert O.cost(A, B, res["best_perm"]) == res["best_cost"]
+
+
+@pytest.mark.parametrize("group", [64, 128, 256])
+def test_ensemble_group_shape_invariance(group):
+    A, B = taixxa(24, 24)
+    p0s = start_perms(24, 3, 0, 20)
+    sch = O.geometric_schedule_for(A, B, p0s[0], 20000)
+    with Q.Solver(A, B, p0s[0]) as s:
+        s.set_option(Q.QAP_OPT_ENSEMBLE_GROUP, group)
+        res = s.ensemble(0, p0s, 20000, _sched(sch), 3, per_chain=True)
+    ref = O.ensemble_run(A, B, p0s, 0, 20000, sch, 3)
+    got = np.array([[r["cost"], r["best_cost"], r["accepted"]] for r in res["per_chain"]])
+    np.testing.assert_array_equal(got, ref[:, :3])
+
+
+# ---------------- full-size configs (launch configuration of bench.py) ----------------
+
+@pytest.mark.slow
+def test_config3_full_size():
+    """BASELINE config 3 (N=100, 1e8) end to end vs the oracle (SCRATCH δ source)."""
+    A, B, p0, cfg = config(3)
+    sch = O.geometric_schedule_for(A, B, p0, cfg["iters"])
+    _compare_run(A, B, p0, cfg["iters"], sch, mode=O.MODE_SCRATCH)
+
+
+@pytest.mark.slow
+def test_config5_full_size_sampled_chains():
+    """BASELINE config 5 (8192 x N=100 x 1e7) on one GPU; sampled chains vs the oracle,
+    argmin consistency and the best permutation's Eq.(1) cost."""
+    A, B, _, cfg = config(5)
+    C = cfg["chains"]
+    p0s = start_perms(100, SA_SEED, 0, C)
+    sch = O.geometric_schedule_for(A, B, p0s[0], cfg["iters"])
+    with Q.Solver(A, B, p0s[0]) as s:
+        res = s.ensemble(0, p0s, cfg["iters"], _sched(sch), SA_SEED, per_chain=True)
+    per = res["per_chain"]
+    best = min(range(C), key=lambda i: (per[i]["best_cost"], i))
+    assert res["best_chain"] == best and res["best_cost"] == per[best]["best_cost"]
+    assert O.cost(A, B, res["best_perm"]) == res["best_cost"]
+    for i in [0, 1, 4095, C - 1]:
+        if per[i]["near_ties"]:
+            continue
+        o = O.Run(A, B, p0s[i], mode=O.MODE_SCRATCH, chain=i).run(0, cfg["iters"], sch, SA_SEED)
+        assert (per[i]["cost"], per[i]["best_cost"], per[i]["accepted"], per[i]["digest"]) == (
+            o["cost"], o["best_cost"], o["accepted"], o["digest"])
