@@ -42,12 +42,20 @@ struct Sched {
     int kind;      // 0 geometric, 1 Lundy-Mees
     double t0;
     double coef;
+    float t0f;     // (float)t0
 };
 
 __device__ __forceinline__ double temperature(const Sched& s, uint64_t k) {
     if (s.kind == 1)
         return __ddiv_rn(s.t0, __dadd_rn(1.0, __dmul_rn(__dmul_rn((double)k, s.coef), s.t0)));
     return __dmul_rn(s.t0, exp(__dmul_rn(s.coef, (double)k)));
+}
+
+// T_k in float, relative error < 2e-6: only brackets decisions (never decides alone).
+__device__ __forceinline__ float temp32(const Sched& s, uint64_t k) {
+    const double x = __dmul_rn(s.coef, (double)k);
+    if (s.kind == 1) return __fdividef(s.t0f, 1.0f + (float)x * s.t0f);
+    return s.t0f * __expf((float)x);
 }
 
 // ---- Eq.(2) acceptance for one candidate in the "live band" (0 < delta <= 38 T):
@@ -59,6 +67,21 @@ __device__ __forceinline__ bool metropolis(int32_t delta, double T, double r, bo
     return acc;
 }
 
+// Fast path: θ = -T ln r in float with a margin far wider than its error; the
+// exact double test decides (and flags near ties) only inside the margin, so
+// the decision equals the double-precision one everywhere.
+__device__ __forceinline__ bool metropolis_fast(int32_t delta, const Sched& s, uint64_t k,
+                                                uint64_t seed, uint32_t chain, bool* near) {
+    const double r = uniform_r(seed, k, chain);
+    const float T = temp32(s, k);
+    const float th = T * -__logf((float)r);
+    const float m = 2e-4f * th + 2e-5f * T;
+    const float df = (float)delta;
+    if (df < th - m) return true;
+    if (df > th + m) return false;
+    return metropolis(delta, temperature(s, k), r, near);
+}
+
 // ---- candidate enumeration: row-major upper triangle (R4, R11)
 __host__ __device__ __forceinline__ int tri_base(int n, int r) { return r * n - (r * (r + 1)) / 2; }
 __host__ __device__ __forceinline__ int tri_index(int n, int r, int s) {
@@ -66,8 +89,8 @@ __host__ __device__ __forceinline__ int tri_index(int n, int r, int s) {
 }
 // q -> (r, s); closed form guess corrected by integer checks.
 __device__ __forceinline__ void tri_pair(int n, int q, int* r, int* s) {
-    const double b = 2.0 * n - 1.0;
-    int rr = (int)floor((b - sqrt(b * b - 8.0 * (double)q)) * 0.5);
+    const int b = 2 * n - 1;                       // b*b - 8q < 2^24: exact in float
+    int rr = (int)((float)b - sqrtf((float)(b * b - 8 * q))) >> 1;
     rr = max(0, min(rr, n - 2));
     while (rr > 0 && tri_base(n, rr) > q) --rr;
     while (rr < n - 2 && tri_base(n, rr + 1) <= q) ++rr;

@@ -32,16 +32,18 @@ struct ChainResult {              // mirrors qap_chain_result
 
 // ---------------- shared-memory layout of one chain group ----------------
 struct GroupLayout {
-    int bp, d, dab, p, bestp, slots, flags, bytes;
+    int bp, d, dab, dg, p, bestp, slots, flags, bytes;
 };
 __host__ __device__ inline int align16(int x) { return (x + 15) & ~15; }
+// dab_bytes: 4 when A and B are both 8-bit (packed int16 pair), else 8
 __host__ __device__ inline GroupLayout group_layout(int n, int ld, int M, int tb_bytes, int nw,
-                                                    bool d_in_smem) {
+                                                    bool d_in_smem, int dab_bytes) {
     GroupLayout L;
     int o = 0;
     L.bp = o;    o = align16(o + n * ld * tb_bytes);
     L.d = o;     o = align16(o + (d_in_smem ? M * 4 : 0));
-    L.dab = o;   o = align16(o + n * 8);
+    L.dab = o;   o = align16(o + n * dab_bytes);
+    L.dg = o;    o = align16(o + n * 4);
     L.p = o;     o = align16(o + n * 2);
     L.bestp = o; o = align16(o + n * 2);
     L.slots = o; o = align16(o + 2 * nw * 16);
@@ -56,7 +58,8 @@ __device__ inline ChainSmem<TA, TB> group_view(unsigned char* base, const GroupL
     ChainSmem<TA, TB> cs;
     cs.Bp = reinterpret_cast<TB*>(base + L.bp);
     cs.D = d_global ? d_global : reinterpret_cast<int32_t*>(base + L.d);
-    cs.dAB = reinterpret_cast<int2*>(base + L.dab);
+    cs.dAB = reinterpret_cast<typename Dab<TA, TB>::T*>(base + L.dab);
+    cs.Dg = reinterpret_cast<int32_t*>(base + L.dg);
     cs.p = reinterpret_cast<uint16_t*>(base + L.p);
     cs.best_p = reinterpret_cast<uint16_t*>(base + L.bestp);
     cs.slots = reinterpret_cast<int4*>(base + L.slots);
@@ -200,7 +203,8 @@ __global__ void __launch_bounds__(NT, 1) k_sa_chain(const ChainArgs a) {
     const int n = a.n, ld = a.ld, M = a.M;
     const int a_bytes = align16(n * ld * (int)sizeof(TA));
     TA* As = reinterpret_cast<TA*>(smem);
-    const GroupLayout L = group_layout(n, ld, M, sizeof(TB), NT / 32, D_SMEM);
+    const GroupLayout L = group_layout(n, ld, M, sizeof(TB), NT / 32, D_SMEM,
+                                       sizeof(typename Dab<TA, TB>::T));
     ChainSmem<TA, TB> cs = group_view<TA, TB>(smem + a_bytes, L, D_SMEM ? nullptr : a.D);
 
     copy_words(As, a.A, n * ld * (int)sizeof(TA), t, NT);
@@ -214,6 +218,8 @@ __global__ void __launch_bounds__(NT, 1) k_sa_chain(const ChainArgs a) {
     build_bprime(cs.Bp, reinterpret_cast<const TB*>(a.B), cs.p, n, ld, t, NT);
     ChainScalars io{a.st->cost, a.st->best_cost, a.st->digest};
     __syncthreads();
+    chain_diag_init<TA, TB, NT>(As, cs, n, ld, t);
+    __syncthreads();
 
     const NearSink sink{a.near_count, a.near_k, a.near_dec, a.near_cap};
     const uint64_t acc = chain_run<TA, TB, NT>(As, cs, n, ld, M, a.k0, a.k_end, a.sch, a.seed, 0u,
@@ -224,7 +230,7 @@ __global__ void __launch_bounds__(NT, 1) k_sa_chain(const ChainArgs a) {
         a.best_p[i] = cs.best_p[i];
     }
     if (D_SMEM) copy_words(a.D, cs.D, M * 4, t, NT);
-    if (t == 0) {
+    if (t == NT - 1) {
         a.st->cost = io.cost;
         a.st->best_cost = io.best;
         a.st->digest = io.digest;
@@ -252,7 +258,8 @@ __global__ void __launch_bounds__(1024, 1) k_ensemble(const EnsArgs a) {
     const int n = a.n, ld = a.ld, M = a.M;
     const int a_bytes = align16(n * ld * (int)sizeof(TA));
     TA* As = reinterpret_cast<TA*>(smem);
-    const GroupLayout L = group_layout(n, ld, M, sizeof(TB), NT / 32, true);
+    const GroupLayout L = group_layout(n, ld, M, sizeof(TB), NT / 32, true,
+                                       sizeof(typename Dab<TA, TB>::T));
     const int g = threadIdx.x / NT, t = threadIdx.x % NT, bar = 1 + g;
     ChainSmem<TA, TB> cs = group_view<TA, TB>(smem + a_bytes + g * L.bytes, L, nullptr);
 
@@ -274,6 +281,7 @@ __global__ void __launch_bounds__(1024, 1) k_ensemble(const EnsArgs a) {
         build_bprime(cs.Bp, reinterpret_cast<const TB*>(a.B), cs.p, n, ld, t, NT);
         group_sync(bar, NT);
         chain_delta_init<TA, TB, NT>(As, cs, n, ld, M, t);
+        chain_diag_init<TA, TB, NT>(As, cs, n, ld, t);
         // C = Eq.(1) = sum_ij A_ij B'_ij
         long long part = 0;
         for (int idx = t; idx < n * n; idx += NT) {
@@ -285,7 +293,7 @@ __global__ void __launch_bounds__(1024, 1) k_ensemble(const EnsArgs a) {
         if ((t & 31) == 0) red[t >> 5] = part;
         group_sync(bar, NT);
         ChainScalars io{0, 0, kDigestSeed};
-        if (t == 0) {
+        if (t == NT - 1) {
             long long c = 0;
             for (int w = 0; w < NT / 32; ++w) c += red[w];
             io.cost = io.best = c;
@@ -296,7 +304,7 @@ __global__ void __launch_bounds__(1024, 1) k_ensemble(const EnsArgs a) {
                                                    a.chain_begin + (unsigned)ci, bar, t, a.wmax, io,
                                                    sink);
         for (int i = t; i < n; i += NT) a.best_perms[(size_t)ci * n + i] = cs.best_p[i];
-        if (t == 0) {
+        if (t == NT - 1) {
             ChainResult r;
             r.cost = io.cost;
             r.best_cost = io.best;

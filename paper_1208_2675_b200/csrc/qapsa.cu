@@ -104,8 +104,10 @@ static std::vector<unsigned char> compact(int n, int ld, const int32_t* X) {
     return out;
 }
 
+static int dab_bytes(const qap_ctx* c) { return (c->ta == 1 && c->tb == 1) ? 4 : 8; }
+
 static int chain_smem_bytes(const qap_ctx* c, int threads, bool d_smem) {
-    const GroupLayout L = group_layout(c->n, c->ld, c->M, c->tb, threads / 32, d_smem);
+    const GroupLayout L = group_layout(c->n, c->ld, c->M, c->tb, threads / 32, d_smem, dab_bytes(c));
     return align16(c->n * c->ld * c->ta) + L.bytes;
 }
 
@@ -124,6 +126,7 @@ static qap_status validate_schedule(qap_ctx* c, const qap_schedule* s, uint64_t 
     const double I1 = (double)(s->total_iters - 1);
     out->kind = s->kind;
     out->t0 = s->t0;
+    out->t0f = (float)s->t0;
     if (s->kind == QAP_COOL_GEOMETRIC)
         out->coef = s->total_iters > 1 ? std::log(s->tf / s->t0) / I1 : 0.0;
     else
@@ -492,7 +495,7 @@ qap_status qap_ensemble_run(qap_ctx* c, uint32_t chain_begin, uint32_t chain_cou
     for (uint32_t i = 0; i < chain_count; ++i)
         if (!is_perm(n, p0s + (size_t)i * n)) return fail(c, QAP_E_DIMENSION, "a start permutation is invalid");
     const int nt = c->ens_group;
-    const GroupLayout L = group_layout(n, c->ld, c->M, c->tb, nt / 32, true);
+    const GroupLayout L = group_layout(n, c->ld, c->M, c->tb, nt / 32, true, dab_bytes(c));
     const int a_bytes = align16(n * c->ld * c->ta);
     int groups = std::min((c->smem_optin - a_bytes) / L.bytes, 1024 / nt);
     if (groups < 1) return fail(c, QAP_E_UNSUPPORTED, "one ensemble chain does not fit on chip");
