@@ -9,6 +9,7 @@ import subprocess
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 LIB = os.path.join(PKG, "libqapsa.so")
+LIB_TIMERS = os.path.join(PKG, "libqapsa_timers.so")   # debug build with in-kernel phase timers
 SOURCES = [os.path.join(PKG, "csrc", "qapsa.cu")]
 DEPS = glob.glob(os.path.join(PKG, "csrc", "*")) + [os.path.join(ROOT, "include", "qapsa.h")]
 
@@ -28,17 +29,20 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def stale() -> bool:
-    if not os.path.exists(LIB):
+def stale(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     return any(os.path.getmtime(f) > t for f in DEPS + SOURCES)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
-        return LIB
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", LIB, *SOURCES]
+def build(force: bool = False, verbose: bool = False, timers: bool = False) -> str:
+    out = LIB_TIMERS if timers else LIB
+    if not force and not stale(out):
+        return out
+    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", out, *SOURCES]
+    if timers:
+        cmd.insert(1, "-DQAPSA_PHASE_TIMERS")
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     res = subprocess.run(cmd, capture_output=True, text=True)
@@ -46,10 +50,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc failed:\n" + res.stderr[-8000:])
     if verbose:
         print(res.stderr)
-    return LIB
+    return out
 
 
 if __name__ == "__main__":
     import sys
-    build(force=True, verbose="-v" in sys.argv)
-    print(LIB)
+    print(build(force=True, verbose="-v" in sys.argv, timers="--timers" in sys.argv))

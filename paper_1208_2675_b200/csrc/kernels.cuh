@@ -32,18 +32,22 @@ struct ChainResult {              // mirrors qap_chain_result
 
 // ---------------- shared-memory layout of one chain group ----------------
 struct GroupLayout {
-    int bp, d, dab, dg, p, bestp, slots, flags, bytes;
+    int bp, d, dab, dg, tr, ts, p, bestp, slots, flags, bytes;
 };
 __host__ __device__ inline int align16(int x) { return (x + 15) & ~15; }
 // dab_bytes: 4 when A and B are both 8-bit (packed int16 pair), else 8
-__host__ __device__ inline GroupLayout group_layout(int n, int ld, int M, int tb_bytes, int nw,
+// nqt: number of Δ quads (quad layout, chain.cuh)
+__host__ __device__ inline GroupLayout group_layout(int n, int ld, int nqt, int tb_bytes, int nw,
                                                     bool d_in_smem, int dab_bytes) {
     GroupLayout L;
+    const int n4 = (n + 3) & ~3;
     int o = 0;
     L.bp = o;    o = align16(o + n * ld * tb_bytes);
-    L.d = o;     o = align16(o + (d_in_smem ? M * 4 : 0));
-    L.dab = o;   o = align16(o + n * dab_bytes);
+    L.d = o;     o = align16(o + (d_in_smem ? nqt * 16 : 0));
+    L.dab = o;   o = align16(o + n4 * dab_bytes);
     L.dg = o;    o = align16(o + n * 4);
+    L.tr = o;    o = align16(o + n4 * 4);
+    L.ts = o;    o = align16(o + n4 * 4);
     L.p = o;     o = align16(o + n * 2);
     L.bestp = o; o = align16(o + n * 2);
     L.slots = o; o = align16(o + 2 * nw * 16);
@@ -60,11 +64,18 @@ __device__ inline ChainSmem<TA, TB> group_view(unsigned char* base, const GroupL
     cs.D = d_global ? d_global : reinterpret_cast<int32_t*>(base + L.d);
     cs.dAB = reinterpret_cast<typename Dab<TA, TB>::T*>(base + L.dab);
     cs.Dg = reinterpret_cast<int32_t*>(base + L.dg);
+    cs.Tr = reinterpret_cast<int32_t*>(base + L.tr);
+    cs.Ts = reinterpret_cast<int32_t*>(base + L.ts);
     cs.p = reinterpret_cast<uint16_t*>(base + L.p);
     cs.best_p = reinterpret_cast<uint16_t*>(base + L.bestp);
     cs.slots = reinterpret_cast<int4*>(base + L.slots);
     cs.flags = reinterpret_cast<int*>(base + L.flags);
     return cs;
+}
+
+// per-CTA prefix: A (n x ld) | rowaddr (n int) | qdesc (nqt uint32)
+__host__ __device__ inline int cta_prefix_bytes(int n, int ld, int ta_bytes, int nqt) {
+    return align16(n * ld * ta_bytes) + align16(n * 4) + align16(nqt * 2);
 }
 
 // cooperative copy of bytes (16-byte aligned, size multiple of 4)
@@ -143,7 +154,8 @@ __global__ void k_cost(const TA* __restrict__ A, const TB* __restrict__ B, const
 // δ(r,s) = 2 [ sum_all k (a_rk - a_sk)(B'_sk - B'_rk) + 2 a_rs B'_rs ]
 template <typename TA, typename TB>
 __global__ void k_delta_init(const TA* __restrict__ A, const TB* __restrict__ B,
-                             const int32_t* __restrict__ p, int n, int ld, int M, int32_t* D) {
+                             const int32_t* __restrict__ p, const int32_t* __restrict__ rowaddr,
+                             int n, int ld, int M, int32_t* D) {
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < M; q += gridDim.x * blockDim.x) {
         int r, s;
         tri_pair(n, q, &r, &s);
@@ -156,7 +168,17 @@ __global__ void k_delta_init(const TA* __restrict__ A, const TB* __restrict__ B,
             const int pk = __ldg(p + k);
             acc += ((int)Ar[k] - (int)As[k]) * ((int)Bs[pk] - (int)Br[pk]);
         }
-        D[q] = 2 * (acc + 2 * (int)Ar[s] * (int)Br[p[s]]);
+        D[rowaddr[r] + s] = 2 * (acc + 2 * (int)Ar[s] * (int)Br[p[s]]);
+    }
+}
+
+// quad layout -> enumeration order (qap_get_state, qap_schedule_bounds)
+__global__ void k_unpad(const int32_t* __restrict__ D, const int32_t* __restrict__ rowaddr, int n,
+                        int M, int32_t* out) {
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < M; q += gridDim.x * blockDim.x) {
+        int r, s;
+        tri_pair(n, q, &r, &s);
+        out[q] = D[rowaddr[r] + s];
     }
 }
 
@@ -185,7 +207,10 @@ struct ChainArgs {
     const void* B;           // n x ld compact
     int32_t* p;              // n
     int32_t* best_p;         // n
-    int32_t* D;              // M (global copy; also the working Δ when !D_SMEM)
+    int32_t* D;              // quad layout (global copy; also the working Δ when !D_SMEM)
+    const int32_t* rowaddr;  // n
+    const uint16_t* qdesc;   // nqt
+    int nqt;
     DevState* st;
     unsigned int* near_count;
     unsigned long long* near_k;
@@ -196,23 +221,34 @@ struct ChainArgs {
     Sched sch;
 };
 
-template <typename TA, typename TB, int NT, bool D_SMEM>
+// NFIX > 0: problem size fixed at compile time (layout offsets and loop bounds fold);
+// NFIX == 0: any n.
+template <typename TA, typename TB, int NT, bool D_SMEM, int NFIX>
 __global__ void __launch_bounds__(NT, 1) k_sa_chain(const ChainArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int t = threadIdx.x;
-    const int n = a.n, ld = a.ld, M = a.M;
+    const int n = NFIX ? NFIX : a.n;
+    const int ld = NFIX ? row_stride(NFIX, sizeof(TA) == 1 && sizeof(TB) == 1) : a.ld;
+    const int M = NFIX ? NFIX * (NFIX - 1) / 2 : a.M;
+    const int nqt = NFIX ? quad_count(NFIX) : a.nqt;
     const int a_bytes = align16(n * ld * (int)sizeof(TA));
     TA* As = reinterpret_cast<TA*>(smem);
-    const GroupLayout L = group_layout(n, ld, M, sizeof(TB), NT / 32, D_SMEM,
+    int32_t* rowaddr = reinterpret_cast<int32_t*>(smem + a_bytes);
+    uint16_t* qdesc = reinterpret_cast<uint16_t*>(smem + a_bytes + align16(n * 4));
+    const GroupLayout L = group_layout(n, ld, nqt, sizeof(TB), NT / 32, D_SMEM,
                                        sizeof(typename Dab<TA, TB>::T));
-    ChainSmem<TA, TB> cs = group_view<TA, TB>(smem + a_bytes, L, D_SMEM ? nullptr : a.D);
+    ChainSmem<TA, TB> cs = group_view<TA, TB>(smem + cta_prefix_bytes(n, ld, sizeof(TA), nqt), L,
+                                              D_SMEM ? nullptr : a.D);
+    const ChainTables tb{rowaddr, qdesc};
 
     copy_words(As, a.A, n * ld * (int)sizeof(TA), t, NT);
+    copy_words(rowaddr, a.rowaddr, n * 4, t, NT);
+    copy_words(qdesc, a.qdesc, (nqt * 2 + 3) & ~3, t, NT);
     for (int i = t; i < n; i += NT) {
         cs.p[i] = (uint16_t)a.p[i];
         cs.best_p[i] = (uint16_t)a.best_p[i];
     }
-    if (D_SMEM) copy_words(cs.D, a.D, M * 4, t, NT);
+    if (D_SMEM) copy_words(cs.D, a.D, nqt * 16, t, NT);
     if (t < 4) cs.flags[t] = 0;
     __syncthreads();
     build_bprime(cs.Bp, reinterpret_cast<const TB*>(a.B), cs.p, n, ld, t, NT);
@@ -222,15 +258,16 @@ __global__ void __launch_bounds__(NT, 1) k_sa_chain(const ChainArgs a) {
     __syncthreads();
 
     const NearSink sink{a.near_count, a.near_k, a.near_dec, a.near_cap};
-    const uint64_t acc = chain_run<TA, TB, NT>(As, cs, n, ld, M, a.k0, a.k_end, a.sch, a.seed, 0u,
-                                               0, t, a.wmax, io, sink);
+    constexpr int QPT = NFIX ? (quad_count(NFIX) + NT - 1) / NT : 0;
+    const uint64_t acc = chain_run<TA, TB, NT, QPT>(As, cs, tb, n, ld, M, nqt, a.k0, a.k_end, a.sch,
+                                                    a.seed, 0u, 0, t, a.wmax, io, sink);
 
     for (int i = t; i < n; i += NT) {
         a.p[i] = cs.p[i];
         a.best_p[i] = cs.best_p[i];
     }
-    if (D_SMEM) copy_words(a.D, cs.D, M * 4, t, NT);
-    if (t == NT - 1) {
+    if (D_SMEM) copy_words(a.D, cs.D, nqt * 16, t, NT);
+    if (t == scalar_tid(NT)) {
         a.st->cost = io.cost;
         a.st->best_cost = io.best;
         a.st->digest = io.digest;
@@ -246,24 +283,36 @@ struct EnsArgs {
     ChainResult* res;            // count
     uint16_t* best_perms;        // count x n
     unsigned int* next_chain;    // work counter
+    const int32_t* rowaddr;      // n
+    const uint16_t* qdesc;       // nqt
+    int nqt;
     int count, n, ld, M, wmax;
     unsigned int chain_begin;
     unsigned long long iters, seed;
     Sched sch;
 };
 
-template <typename TA, typename TB, int NT>
+template <typename TA, typename TB, int NT, int NFIX>
 __global__ void __launch_bounds__(1024, 1) k_ensemble(const EnsArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
-    const int n = a.n, ld = a.ld, M = a.M;
+    const int n = NFIX ? NFIX : a.n;
+    const int ld = NFIX ? row_stride(NFIX, sizeof(TA) == 1 && sizeof(TB) == 1) : a.ld;
+    const int M = NFIX ? NFIX * (NFIX - 1) / 2 : a.M;
+    const int nqt = NFIX ? quad_count(NFIX) : a.nqt;
     const int a_bytes = align16(n * ld * (int)sizeof(TA));
     TA* As = reinterpret_cast<TA*>(smem);
-    const GroupLayout L = group_layout(n, ld, M, sizeof(TB), NT / 32, true,
+    int32_t* rowaddr = reinterpret_cast<int32_t*>(smem + a_bytes);
+    uint16_t* qdesc = reinterpret_cast<uint16_t*>(smem + a_bytes + align16(n * 4));
+    const GroupLayout L = group_layout(n, ld, nqt, sizeof(TB), NT / 32, true,
                                        sizeof(typename Dab<TA, TB>::T));
     const int g = threadIdx.x / NT, t = threadIdx.x % NT, bar = 1 + g;
-    ChainSmem<TA, TB> cs = group_view<TA, TB>(smem + a_bytes + g * L.bytes, L, nullptr);
+    ChainSmem<TA, TB> cs =
+        group_view<TA, TB>(smem + cta_prefix_bytes(n, ld, sizeof(TA), nqt) + g * L.bytes, L, nullptr);
+    const ChainTables tb{rowaddr, qdesc};
 
     copy_words(As, a.A, n * ld * (int)sizeof(TA), threadIdx.x, blockDim.x);
+    copy_words(rowaddr, a.rowaddr, n * 4, threadIdx.x, blockDim.x);
+    copy_words(qdesc, a.qdesc, (nqt * 2 + 3) & ~3, threadIdx.x, blockDim.x);
     __syncthreads();
 
     for (;;) {
@@ -280,7 +329,7 @@ __global__ void __launch_bounds__(1024, 1) k_ensemble(const EnsArgs a) {
         group_sync(bar, NT);
         build_bprime(cs.Bp, reinterpret_cast<const TB*>(a.B), cs.p, n, ld, t, NT);
         group_sync(bar, NT);
-        chain_delta_init<TA, TB, NT>(As, cs, n, ld, M, t);
+        chain_delta_init<TA, TB, NT>(As, cs, tb, n, ld, M, t);
         chain_diag_init<TA, TB, NT>(As, cs, n, ld, t);
         // C = Eq.(1) = sum_ij A_ij B'_ij
         long long part = 0;
@@ -293,18 +342,16 @@ __global__ void __launch_bounds__(1024, 1) k_ensemble(const EnsArgs a) {
         if ((t & 31) == 0) red[t >> 5] = part;
         group_sync(bar, NT);
         ChainScalars io{0, 0, kDigestSeed};
-        if (t == NT - 1) {
-            long long c = 0;
-            for (int w = 0; w < NT / 32; ++w) c += red[w];
-            io.cost = io.best = c;
-        }
+        for (int w = 0; w < NT / 32; ++w) io.cost += red[w];
+        io.best = io.cost;
         group_sync(bar, NT);
         const NearSink sink{nullptr, nullptr, nullptr, 0};
-        const uint64_t acc = chain_run<TA, TB, NT>(As, cs, n, ld, M, 0ull, a.iters, a.sch, a.seed,
-                                                   a.chain_begin + (unsigned)ci, bar, t, a.wmax, io,
-                                                   sink);
+        constexpr int QPT = NFIX ? (quad_count(NFIX) + NT - 1) / NT : 0;
+        const uint64_t acc = chain_run<TA, TB, NT, QPT>(As, cs, tb, n, ld, M, nqt, 0ull, a.iters, a.sch,
+                                                   a.seed, a.chain_begin + (unsigned)ci, bar, t,
+                                                   a.wmax, io, sink);
         for (int i = t; i < n; i += NT) a.best_perms[(size_t)ci * n + i] = cs.best_p[i];
-        if (t == NT - 1) {
+        if (t == scalar_tid(NT)) {
             ChainResult r;
             r.cost = io.cost;
             r.best_cost = io.best;

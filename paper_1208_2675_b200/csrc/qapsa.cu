@@ -26,6 +26,10 @@ struct qap_ctx {
     void* dA = nullptr;
     void* dB = nullptr;
     int32_t *dp0 = nullptr, *dp = nullptr, *dbest = nullptr, *dD = nullptr, *dperm = nullptr;
+    int32_t* dDlin = nullptr;           // M, enumeration-order copy of Δ
+    int32_t* drowaddr = nullptr;        // n, quad layout row addresses
+    uint16_t* dqdesc = nullptr;         // nqt, quad descriptors
+    int nqt = 0;
     DevState* dst = nullptr;
     unsigned int* dnear_count = nullptr;
     unsigned long long* dnear_k = nullptr;
@@ -40,7 +44,7 @@ struct qap_ctx {
     bool delta_valid = false;
     bool sticky = false;
     std::string err;
-    int wmax = 1024, threads = 1024, force_global = 0, ens_group = 128;
+    int wmax = 1024, threads = 0 /* auto */, force_global = 0, ens_group = 128;
     int smem_optin = 0, num_sms = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     float last_ms = 0.f;
@@ -107,8 +111,20 @@ static std::vector<unsigned char> compact(int n, int ld, const int32_t* X) {
 static int dab_bytes(const qap_ctx* c) { return (c->ta == 1 && c->tb == 1) ? 4 : 8; }
 
 static int chain_smem_bytes(const qap_ctx* c, int threads, bool d_smem) {
-    const GroupLayout L = group_layout(c->n, c->ld, c->M, c->tb, threads / 32, d_smem, dab_bytes(c));
-    return align16(c->n * c->ld * c->ta) + L.bytes;
+    const GroupLayout L = group_layout(c->n, c->ld, c->nqt, c->tb, threads / 32, d_smem, dab_bytes(c));
+    return cta_prefix_bytes(c->n, c->ld, c->ta, c->nqt) + L.bytes;
+}
+
+// Quad layout of Δ (chain.cuh): row u keeps column quads floor((u+1)/4) .. ceil(n/4)-1.
+static void quad_tables(int n, std::vector<int32_t>* rowaddr, std::vector<uint16_t>* qdesc) {
+    const int NQ = (n + 3) / 4;
+    rowaddr->assign(n, 0);
+    qdesc->clear();
+    for (int u = 0; u + 1 < n; ++u) {
+        const int j0 = (u + 1) / 4;
+        (*rowaddr)[u] = 4 * (int)qdesc->size() - 4 * j0;
+        for (int j = j0; j < NQ; ++j) qdesc->push_back((uint16_t)(u | (j << 9)));
+    }
 }
 
 static qap_status validate_schedule(qap_ctx* c, const qap_schedule* s, uint64_t k0, uint64_t iters,
@@ -159,7 +175,8 @@ const char* qap_last_error(const qap_ctx* ctx) {
 
 void qap_destroy(qap_ctx* c) {
     if (!c) return;
-    void* ptrs[] = {c->dA, c->dB, c->dp0, c->dp, c->dbest, c->dD, c->dperm, c->dst, c->dnear_count,
+    void* ptrs[] = {c->dA, c->dB, c->dp0, c->dp, c->dbest, c->dD, c->dperm, c->dDlin, c->drowaddr,
+                    c->dqdesc, c->dst, c->dnear_count,
                     c->dnear_k, c->dnear_dec, c->dscratch, c->ens_p0, c->ens_res, c->ens_best,
                     c->ens_counter};
     for (void* p : ptrs)
@@ -209,13 +226,17 @@ qap_status qap_create(int32_t n, const int32_t* A, const int32_t* B, const int32
 
     c = new qap_ctx();
     c->n = n;
-    c->ld = (n + 3) & ~3;
+    c->ld = row_stride(n, maxA <= 255 && maxB <= 255);
     c->M = n * (n - 1) / 2;
     c->dev = device;
     c->stream = (cudaStream_t)stream;
     c->ta = maxA <= 255 ? 1 : 2;
     c->tb = maxB <= 255 ? 1 : 2;
     c->smem_optin = (int)prop.sharedMemPerBlockOptin;
+    std::vector<int32_t> hrow;
+    std::vector<uint16_t> hq;
+    quad_tables(n, &hrow, &hq);
+    c->nqt = (int)hq.size();
     c->num_sms = prop.multiProcessorCount;
     if (cudaSetDevice(device) != cudaSuccess) {
         delete c;
@@ -240,7 +261,10 @@ qap_status qap_create(int32_t n, const int32_t* A, const int32_t* B, const int32
     alloc((void**)&c->dp, n * 4);
     alloc((void**)&c->dbest, n * 4);
     alloc((void**)&c->dperm, n * 4);
-    alloc((void**)&c->dD, (size_t)(c->M + 4) * 4);
+    alloc((void**)&c->dD, (size_t)c->nqt * 16 + 16);
+    alloc((void**)&c->dDlin, (size_t)c->M * 4);
+    alloc((void**)&c->drowaddr, (size_t)n * 4);
+    alloc((void**)&c->dqdesc, (size_t)c->nqt * 4 + 4);
     alloc((void**)&c->dst, sizeof(DevState));
     alloc((void**)&c->dnear_count, sizeof(unsigned int));
     alloc((void**)&c->dnear_k, QAP_NEAR_LOG_CAP * sizeof(unsigned long long));
@@ -257,6 +281,9 @@ qap_status qap_create(int32_t n, const int32_t* A, const int32_t* B, const int32
     cudaError_t e = cudaMemcpyAsync(c->dA, hA.data(), nA, cudaMemcpyHostToDevice, c->stream);
     if (e == cudaSuccess) e = cudaMemcpyAsync(c->dB, hB.data(), nB, cudaMemcpyHostToDevice, c->stream);
     if (e == cudaSuccess) e = cudaMemcpyAsync(c->dp0, p0, n * 4, cudaMemcpyHostToDevice, c->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(c->drowaddr, hrow.data(), n * 4, cudaMemcpyHostToDevice, c->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(c->dqdesc, hq.data(), hq.size() * 2, cudaMemcpyHostToDevice, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);   // host tables go out of scope
     if (e != cudaSuccess) {
         std::string m = cudaGetErrorString(e);
         qap_destroy(c);
@@ -295,14 +322,15 @@ qap_status qap_delta_init(qap_ctx* c) {
     CHECK_CTX(c);
     CU(cudaSetDevice(c->dev));
     const int threads = 256, blocks = (c->M + threads - 1) / threads;
+    CU(cudaMemsetAsync(c->dD, 0, (size_t)c->nqt * 16, c->stream));   // dead slots of the quad layout
     if (c->ta == 1 && c->tb == 1)
-        k_delta_init<uint8_t, uint8_t><<<blocks, threads, 0, c->stream>>>((const uint8_t*)c->dA, (const uint8_t*)c->dB, c->dp, c->n, c->ld, c->M, c->dD);
+        k_delta_init<uint8_t, uint8_t><<<blocks, threads, 0, c->stream>>>((const uint8_t*)c->dA, (const uint8_t*)c->dB, c->dp, c->drowaddr, c->n, c->ld, c->M, c->dD);
     else if (c->ta == 1)
-        k_delta_init<uint8_t, uint16_t><<<blocks, threads, 0, c->stream>>>((const uint8_t*)c->dA, (const uint16_t*)c->dB, c->dp, c->n, c->ld, c->M, c->dD);
+        k_delta_init<uint8_t, uint16_t><<<blocks, threads, 0, c->stream>>>((const uint8_t*)c->dA, (const uint16_t*)c->dB, c->dp, c->drowaddr, c->n, c->ld, c->M, c->dD);
     else if (c->tb == 1)
-        k_delta_init<uint16_t, uint8_t><<<blocks, threads, 0, c->stream>>>((const uint16_t*)c->dA, (const uint8_t*)c->dB, c->dp, c->n, c->ld, c->M, c->dD);
+        k_delta_init<uint16_t, uint8_t><<<blocks, threads, 0, c->stream>>>((const uint16_t*)c->dA, (const uint8_t*)c->dB, c->dp, c->drowaddr, c->n, c->ld, c->M, c->dD);
     else
-        k_delta_init<uint16_t, uint16_t><<<blocks, threads, 0, c->stream>>>((const uint16_t*)c->dA, (const uint16_t*)c->dB, c->dp, c->n, c->ld, c->M, c->dD);
+        k_delta_init<uint16_t, uint16_t><<<blocks, threads, 0, c->stream>>>((const uint16_t*)c->dA, (const uint16_t*)c->dB, c->dp, c->drowaddr, c->n, c->ld, c->M, c->dD);
     CU(cudaGetLastError());
     CU(cudaStreamSynchronize(c->stream));
     c->delta_valid = true;
@@ -312,20 +340,61 @@ qap_status qap_delta_init(qap_ctx* c) {
 
 }  // extern "C"
 
-template <typename TA, typename TB, int NT, bool DS>
+template <typename TA, typename TB, int NT, bool DS, int NFIX>
 static cudaError_t launch_chain_t(qap_ctx* c, const ChainArgs& a, int smem) {
-    auto kern = k_sa_chain<TA, TB, NT, DS>;
+    auto kern = k_sa_chain<TA, TB, NT, DS, NFIX>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     kern<<<1, NT, smem, c->stream>>>(a);
     return cudaGetLastError();
 }
 
-template <typename TA, typename TB>
-static cudaError_t launch_chain_tt(qap_ctx* c, const ChainArgs& a, int threads, bool ds, int smem) {
-    if (threads == 1024) return ds ? launch_chain_t<TA, TB, 1024, true>(c, a, smem) : launch_chain_t<TA, TB, 1024, false>(c, a, smem);
-    if (threads == 512) return ds ? launch_chain_t<TA, TB, 512, true>(c, a, smem) : launch_chain_t<TA, TB, 512, false>(c, a, smem);
-    return ds ? launch_chain_t<TA, TB, 256, true>(c, a, smem) : launch_chain_t<TA, TB, 256, false>(c, a, smem);
+template <typename TA, typename TB, int NT>
+static cudaError_t launch_generic(qap_ctx* c, const ChainArgs& a, bool ds, int smem) {
+    return ds ? launch_chain_t<TA, TB, NT, true, 0>(c, a, smem)
+              : launch_chain_t<TA, TB, NT, false, 0>(c, a, smem);
+}
+
+// Threads of the single-chain CTA: enough for 4 lanes per touching v and <= 3 quads per thread.
+static int auto_threads(const qap_ctx* c) {
+    int nt = 64;
+    while (nt < 1024 && (nt < 4 * c->n || 3 * nt < c->nqt)) nt *= 2;
+    return nt;
+}
+
+// Specialised instances (problem size fixed at compile time) for the BASELINE
+// configurations; everything else runs the generic instance of the same code.
+static cudaError_t launch_chain(qap_ctx* c, const ChainArgs& a, int threads, bool explicit_threads,
+                                bool ds, int smem) {
+    if (!explicit_threads) {
+        if (c->ta == 1 && c->tb == 1 && ds) {
+            if (c->n == 12 && threads == 64) return launch_chain_t<uint8_t, uint8_t, 64, true, 12>(c, a, smem);
+            if (c->n == 50 && threads == 256) return launch_chain_t<uint8_t, uint8_t, 256, true, 50>(c, a, smem);
+            if (c->n == 100 && threads == 512) return launch_chain_t<uint8_t, uint8_t, 512, true, 100>(c, a, smem);
+        }
+        if (c->ta == 1 && c->tb == 2 && !ds && c->n == 256 && threads == 1024)
+            return launch_chain_t<uint8_t, uint16_t, 1024, false, 256>(c, a, smem);
+    }
+    if (c->ta == 1 && c->tb == 1) {
+        switch (threads) {
+            case 64: return launch_generic<uint8_t, uint8_t, 64>(c, a, ds, smem);
+            case 128: return launch_generic<uint8_t, uint8_t, 128>(c, a, ds, smem);
+            case 256: return launch_generic<uint8_t, uint8_t, 256>(c, a, ds, smem);
+            case 512: return launch_generic<uint8_t, uint8_t, 512>(c, a, ds, smem);
+            default: return launch_generic<uint8_t, uint8_t, 1024>(c, a, ds, smem);
+        }
+    }
+    if (c->ta == 1) return threads == 256 ? launch_generic<uint8_t, uint16_t, 256>(c, a, ds, smem)
+                                          : launch_generic<uint8_t, uint16_t, 1024>(c, a, ds, smem);
+    if (c->tb == 1) return launch_generic<uint16_t, uint8_t, 1024>(c, a, ds, smem);
+    return launch_generic<uint16_t, uint16_t, 1024>(c, a, ds, smem);
+}
+
+// the instance launch_chain will actually run (for the shared-memory size)
+static int effective_threads(const qap_ctx* c, int threads) {
+    if (c->ta == 1 && c->tb == 1) return threads;
+    if (c->ta == 1) return threads == 256 ? 256 : 1024;
+    return 1024;
 }
 
 extern "C" {
@@ -344,25 +413,22 @@ qap_status qap_sa_run(qap_ctx* c, uint64_t k0, uint64_t iters, const qap_schedul
     CU(cudaMemcpyAsync(&before, c->dst, sizeof before, cudaMemcpyDeviceToHost, c->stream));
     CU(cudaMemcpyAsync(&near_before, c->dnear_count, sizeof near_before, cudaMemcpyDeviceToHost, c->stream));
 
-    int threads = c->threads;
+    const bool explicit_threads = c->threads != 0;
+    const int threads = effective_threads(c, explicit_threads ? c->threads : auto_threads(c));
     bool ds = !c->force_global && chain_smem_bytes(c, threads, true) <= c->smem_optin;
     const int smem = chain_smem_bytes(c, threads, ds);
     if (smem > c->smem_optin) return fail(c, QAP_E_UNSUPPORTED, "chain state does not fit on chip");
 
     ChainArgs a;
     a.A = c->dA; a.B = c->dB; a.p = c->dp; a.best_p = c->dbest; a.D = c->dD; a.st = c->dst;
+    a.rowaddr = c->drowaddr; a.qdesc = c->dqdesc; a.nqt = c->nqt;
     a.near_count = c->dnear_count; a.near_k = c->dnear_k; a.near_dec = c->dnear_dec;
     a.near_cap = QAP_NEAR_LOG_CAP;
     a.n = c->n; a.ld = c->ld; a.M = c->M; a.wmax = std::min(c->wmax, threads);
     a.k0 = k0; a.k_end = k0 + iters; a.seed = seed; a.sch = sch;
 
     CU(cudaEventRecord(c->ev0, c->stream));
-    cudaError_t e;
-    if (c->ta == 1 && c->tb == 1) e = launch_chain_tt<uint8_t, uint8_t>(c, a, threads, ds, smem);
-    else if (c->ta == 1) e = launch_chain_tt<uint8_t, uint16_t>(c, a, threads, ds, smem);
-    else if (c->tb == 1) e = launch_chain_tt<uint16_t, uint8_t>(c, a, threads, ds, smem);
-    else e = launch_chain_tt<uint16_t, uint16_t>(c, a, threads, ds, smem);
-    CU(e);
+    CU(launch_chain(c, a, threads, explicit_threads, ds, smem));
     CU(cudaEventRecord(c->ev1, c->stream));
     DevState after;
     unsigned int near_after = 0;
@@ -415,7 +481,11 @@ qap_status qap_get_state(qap_ctx* c, int32_t* perm, int32_t* best_perm, int32_t*
     CU(cudaSetDevice(c->dev));
     if (perm) CU(cudaMemcpyAsync(perm, c->dp, c->n * 4, cudaMemcpyDeviceToHost, c->stream));
     if (best_perm) CU(cudaMemcpyAsync(best_perm, c->dbest, c->n * 4, cudaMemcpyDeviceToHost, c->stream));
-    if (delta) CU(cudaMemcpyAsync(delta, c->dD, (size_t)c->M * 4, cudaMemcpyDeviceToHost, c->stream));
+    if (delta) {
+        k_unpad<<<(c->M + 255) / 256, 256, 0, c->stream>>>(c->dD, c->drowaddr, c->n, c->M, c->dDlin);
+        CU(cudaGetLastError());
+        CU(cudaMemcpyAsync(delta, c->dDlin, (size_t)c->M * 4, cudaMemcpyDeviceToHost, c->stream));
+    }
     CU(cudaStreamSynchronize(c->stream));
     c->last_launches = 0;
     return QAP_OK;
@@ -444,7 +514,8 @@ qap_status qap_schedule_bounds(qap_ctx* c, double* t0, double* tf) {
     if (!t0 || !tf) return fail(c, QAP_E_INVALID_ARG, "NULL output");
     if (!c->delta_valid) return fail(c, QAP_E_STATE, "Δ not initialised");
     CU(cudaSetDevice(c->dev));
-    k_delta_bounds<<<1, 1024, 0, c->stream>>>(c->dD, c->M, reinterpret_cast<int*>(c->dscratch));
+    k_unpad<<<(c->M + 255) / 256, 256, 0, c->stream>>>(c->dD, c->drowaddr, c->n, c->M, c->dDlin);
+    k_delta_bounds<<<1, 1024, 0, c->stream>>>(c->dDlin, c->M, reinterpret_cast<int*>(c->dscratch));
     CU(cudaGetLastError());
     int mm[2];
     CU(cudaMemcpyAsync(mm, c->dscratch, sizeof mm, cudaMemcpyDeviceToHost, c->stream));
@@ -462,9 +533,9 @@ qap_status qap_schedule_bounds(qap_ctx* c, double* t0, double* tf) {
 
 }  // extern "C"
 
-template <typename TA, typename TB, int NT>
+template <typename TA, typename TB, int NT, int NFIX>
 static cudaError_t launch_ens_t(qap_ctx* c, const EnsArgs& a, int groups, int smem) {
-    auto kern = k_ensemble<TA, TB, NT>;
+    auto kern = k_ensemble<TA, TB, NT, NFIX>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     const int blocks = std::min(c->num_sms, (a.count + groups - 1) / groups);
@@ -472,11 +543,16 @@ static cudaError_t launch_ens_t(qap_ctx* c, const EnsArgs& a, int groups, int sm
     return cudaGetLastError();
 }
 
-template <typename TA, typename TB>
-static cudaError_t launch_ens_tt(qap_ctx* c, const EnsArgs& a, int nt, int groups, int smem) {
-    if (nt == 256) return launch_ens_t<TA, TB, 256>(c, a, groups, smem);
-    if (nt == 64) return launch_ens_t<TA, TB, 64>(c, a, groups, smem);
-    return launch_ens_t<TA, TB, 128>(c, a, groups, smem);
+static cudaError_t launch_ens(qap_ctx* c, const EnsArgs& a, int nt, int groups, int smem) {
+    if (c->ta == 1 && c->tb == 1) {
+        if (nt == 128 && c->n == 100) return launch_ens_t<uint8_t, uint8_t, 128, 100>(c, a, groups, smem);
+        if (nt == 256) return launch_ens_t<uint8_t, uint8_t, 256, 0>(c, a, groups, smem);
+        if (nt == 64) return launch_ens_t<uint8_t, uint8_t, 64, 0>(c, a, groups, smem);
+        return launch_ens_t<uint8_t, uint8_t, 128, 0>(c, a, groups, smem);
+    }
+    if (c->ta == 1) return launch_ens_t<uint8_t, uint16_t, 128, 0>(c, a, groups, smem);
+    if (c->tb == 1) return launch_ens_t<uint16_t, uint8_t, 128, 0>(c, a, groups, smem);
+    return launch_ens_t<uint16_t, uint16_t, 128, 0>(c, a, groups, smem);
 }
 
 extern "C" {
@@ -494,9 +570,9 @@ qap_status qap_ensemble_run(qap_ctx* c, uint32_t chain_begin, uint32_t chain_cou
     const int n = c->n;
     for (uint32_t i = 0; i < chain_count; ++i)
         if (!is_perm(n, p0s + (size_t)i * n)) return fail(c, QAP_E_DIMENSION, "a start permutation is invalid");
-    const int nt = c->ens_group;
-    const GroupLayout L = group_layout(n, c->ld, c->M, c->tb, nt / 32, true, dab_bytes(c));
-    const int a_bytes = align16(n * c->ld * c->ta);
+    const int nt = (c->ta == 1 && c->tb == 1) ? c->ens_group : 128;
+    const GroupLayout L = group_layout(n, c->ld, c->nqt, c->tb, nt / 32, true, dab_bytes(c));
+    const int a_bytes = cta_prefix_bytes(n, c->ld, c->ta, c->nqt);
     int groups = std::min((c->smem_optin - a_bytes) / L.bytes, 1024 / nt);
     if (groups < 1) return fail(c, QAP_E_UNSUPPORTED, "one ensemble chain does not fit on chip");
     const int smem = a_bytes + groups * L.bytes;
@@ -518,14 +594,10 @@ qap_status qap_ensemble_run(qap_ctx* c, uint32_t chain_begin, uint32_t chain_cou
     EnsArgs a;
     a.A = c->dA; a.B = c->dB; a.p0s = c->ens_p0; a.res = c->ens_res; a.best_perms = c->ens_best;
     a.next_chain = c->ens_counter; a.count = (int)chain_count; a.n = n; a.ld = c->ld; a.M = c->M;
+    a.rowaddr = c->drowaddr; a.qdesc = c->dqdesc; a.nqt = c->nqt;
     a.wmax = std::min(c->wmax, nt); a.chain_begin = chain_begin; a.iters = iters; a.seed = seed; a.sch = sch;
     CU(cudaEventRecord(c->ev0, c->stream));
-    cudaError_t e;
-    if (c->ta == 1 && c->tb == 1) e = launch_ens_tt<uint8_t, uint8_t>(c, a, nt, groups, smem);
-    else if (c->ta == 1) e = launch_ens_tt<uint8_t, uint16_t>(c, a, nt, groups, smem);
-    else if (c->tb == 1) e = launch_ens_tt<uint16_t, uint8_t>(c, a, nt, groups, smem);
-    else e = launch_ens_tt<uint16_t, uint16_t>(c, a, nt, groups, smem);
-    CU(e);
+    CU(launch_ens(c, a, nt, groups, smem));
     CU(cudaEventRecord(c->ev1, c->stream));
     k_ens_reduce<<<1, 1024, 0, c->stream>>>(c->ens_res, (int)chain_count, c->dscratch);
     CU(cudaGetLastError());
@@ -555,6 +627,15 @@ qap_status qap_ensemble_run(qap_ctx* c, uint32_t chain_begin, uint32_t chain_cou
     return QAP_OK;
 }
 
+#ifdef QAPSA_PHASE_TIMERS
+// debug build only (not part of include/qapsa.h): read-and-clear the phase cycle counters
+int qapsa_debug_phase_cycles(unsigned long long* out8) {
+    if (cudaMemcpyFromSymbol(out8, g_phase_cycles, 8 * sizeof(unsigned long long)) != cudaSuccess) return 1;
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    return cudaMemcpyToSymbol(g_phase_cycles, z, sizeof z) != cudaSuccess;
+}
+#endif
+
 qap_status qap_set_option(qap_ctx* c, int32_t key, int64_t value) {
     CHECK_CTX(c);
     switch (key) {
@@ -563,7 +644,8 @@ qap_status qap_set_option(qap_ctx* c, int32_t key, int64_t value) {
             c->wmax = (int)value;
             return QAP_OK;
         case QAP_OPT_THREADS:
-            if (value != 256 && value != 512 && value != 1024) return fail(c, QAP_E_INVALID_ARG, "threads must be 256, 512 or 1024");
+            if (value != 0 && value != 64 && value != 128 && value != 256 && value != 512 && value != 1024)
+                return fail(c, QAP_E_INVALID_ARG, "threads must be 0 (auto), 64, 128, 256, 512 or 1024");
             c->threads = (int)value;
             return QAP_OK;
         case QAP_OPT_FORCE_GLOBAL_DELTA:

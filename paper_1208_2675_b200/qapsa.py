@@ -14,7 +14,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libqapsa.so")
+LIB_PATH = os.environ.get("QAPSA_LIB") or os.path.join(_PKG, "libqapsa.so")
 
 QAP_OK = 0
 STATUS = {0: "QAP_OK", 1: "QAP_E_INVALID_ARG", 2: "QAP_E_DIMENSION", 3: "QAP_E_UNSUPPORTED",
@@ -63,7 +63,7 @@ def lib(build_if_missing: bool = True):
     global _lib
     if _lib is not None:
         return _lib
-    if build_if_missing:
+    if build_if_missing and "QAPSA_LIB" not in os.environ:
         from . import _build
         _build.build()
     if not os.path.exists(LIB_PATH):

@@ -1,0 +1,31 @@
+"""Per-phase cycle breakdown of the single-chain kernel (debug build libqapsa_timers.so)."""
+import ctypes as C
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+os.environ["QAPSA_LIB"] = os.path.join(ROOT, "paper_1208_2675_b200", "libqapsa_timers.so")
+from paper_1208_2675_b200 import qapsa as Q  # noqa: E402
+from qap_inputs import SA_SEED, config  # noqa: E402
+
+iters = int(float(sys.argv[1])) if len(sys.argv) > 1 else 10**6
+threads = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+A, B, p0, cfg = config(3)
+s = Q.Solver(A, B, p0)
+if threads:
+    s.set_option(Q.QAP_OPT_THREADS, threads)
+s.delta_init()
+t0, tf = s.schedule_bounds()
+sch = Q.make_schedule(0, t0, tf, cfg["iters"])
+L = Q.lib()
+buf = (C.c_ulonglong * 8)()
+L.qapsa_debug_phase_cycles(buf)
+g = s.run(0, iters, sch, SA_SEED)
+ms, _ = s.last_kernel_time()
+L.qapsa_debug_phase_cycles(buf)
+w_acc, w_no, S, U, nacc, nno = buf[0], buf[1], buf[2], buf[3], buf[4], buf[5]
+print(f"iters {iters:.0e} threads {threads or 'auto'}: {ms:.1f} ms, accepts {g['accepted']}, "
+      f"{ms*1e6/max(1,g['accepted']):.0f} ns/accept")
+print(f"  per accept: W {w_acc/max(1,nacc):.0f} clk, S {S/max(1,nacc):.0f} clk, U {U/max(1,nacc):.0f} clk;"
+      f"  non-accepting windows: {nno} x {w_no/max(1,nno):.0f} clk")
