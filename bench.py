@@ -315,51 +315,46 @@ def run_ours(args):
 
 
 def run_ensemble(args, Q, s, pg, ws, rank, sch_t0tf):
-    """BASELINE config 5: 8192 chains x 1e7 iterations split over ranks + NCCL min-reduce."""
+    """BASELINE config 5: 8192 chains x 1e7 iterations split over ranks + NCCL min-reduce,
+    through the product's distributed driver (paper_1208_2675_b200.dist)."""
     import torch
+    from paper_1208_2675_b200.dist import chain_range, ensemble_distributed
     A, B, _, cfg = config(5)
     C, I = args.ens_chains, args.ens_iters
     n = cfg["n"]
-    per = C // ws
-    begin = rank * per
-    count = per if rank < ws - 1 else C - begin
-    p0s = start_perms(n, SA_SEED, begin, count)
     t0, tf = sch_t0tf
     sch = Q.make_schedule(Q.QAP_COOL_GEOMETRIC, t0, tf, I)
     warm = Q.make_schedule(Q.QAP_COOL_GEOMETRIC, t0, tf, 10**5)
+    begin, end = chain_range(rank, ws, C)
+    p0_local = start_perms(n, SA_SEED, begin, end - begin)
     for _ in range(args.warmup):
-        s.ensemble(begin, p0s[: min(count, 1024)], 10**5, warm, SA_SEED)
+        s.ensemble(begin, p0_local[: min(end - begin, 1024)], 10**5, warm, SA_SEED)
+    kern = {}
+
+    def runner(A_, B_, b, p0s, iters, schedule, seed):
+        res = s.ensemble(b, p0s, iters, schedule, seed)
+        kern["ms"] = s.last_kernel_time()[0]
+        return res
+
     if pg:
         pg.barrier()
     torch.cuda.synchronize()
     t = time.perf_counter()
-    res = s.ensemble(begin, p0s, I, sch, SA_SEED)
-    kms, _ = s.last_kernel_time()
-    # NCCL min-reduce of (best_cost, chain) and broadcast of the best permutation
-    key = torch.tensor([res["best_cost"] * C + res["best_chain"]], device="cuda", dtype=torch.int64)
-    if pg:
-        pg.all_reduce(key, op=pg.ReduceOp.MIN)
-    best_cost, best_chain = divmod(int(key.item()), C)
-    perm = torch.tensor(res["best_perm"], device="cuda", dtype=torch.int32)
-    if pg:
-        owner = torch.tensor([rank if res["best_chain"] == best_chain else ws], device="cuda")
-        pg.all_reduce(owner, op=pg.ReduceOp.MIN)
-        pg.broadcast(perm, src=int(owner.item()))
+    res = ensemble_distributed(A, B, C, I, sch, SA_SEED,
+                               p0_fn=lambda b, c: p0_local if b == begin else start_perms(n, SA_SEED, b, c),
+                               local_runner=runner)
     torch.cuda.synchronize()
     wall_ms = 1e3 * (time.perf_counter() - t)
-    tt = torch.tensor([kms, wall_ms], device="cuda", dtype=torch.float64)
+    tt = torch.tensor([kern.get("ms", 0.0), wall_ms], device="cuda", dtype=torch.float64)
     if pg:
         pg.all_reduce(tt, op=pg.ReduceOp.MAX)
     kms, wall_ms = float(tt[0]), float(tt[1])
-    acc = torch.tensor([res["stats"]["accepted"]], device="cuda", dtype=torch.int64)
-    if pg:
-        pg.all_reduce(acc)
     return {"metric": "chain-iterations/s (8192 x N=100 chains)", "unit": "chain-iterations/s",
             "value": C * I / (kms / 1e3), "value_incl_reduce": C * I / (wall_ms / 1e3),
             "kernel_ms": kms, "chains": C, "iters_per_chain": I, "n_gpus": ws,
-            "scaling": "strong", "best_cost": best_cost, "best_chain": best_chain,
-            "accepted": int(acc.item()), "warmup": f"{args.warmup} x (<=1024 chains x 1e5 it)",
-            "timed_runs": 1}
+            "scaling": "strong", "best_cost": res.best_cost, "best_chain": res.best_chain,
+            "accepted": res.accepted, "near_ties": res.near_ties,
+            "warmup": f"{args.warmup} x (<=1024 chains x 1e5 it)", "timed_runs": 1}
 
 
 def main():
