@@ -1,31 +1,31 @@
 // chain.cuh -- one Δ-matrix SA chain run by a group of NT threads that keeps
 // its whole state in shared memory (Δ may instead live in global memory / L2).
 //
-// Per accepted swap (r,s) the group goes through three phases separated by
+// Per accepted swap (r,s) the group goes through two phases separated by
 // named barriers ("a synchronization mechanism is needed"; the group is
 // inside one CTA, so a hardware barrier suffices):
-//   W  window: thread t tests candidate k+t against Eq.(2) with an
-//      address and a threshold θ = -T ln r prepared off the critical path
-//      (in U of the previous accept, or speculatively in the previous window);
-//      warp vote (__ballot_sync/__ffs) + cross-warp min picks the first
-//      accepted candidate ("the swap which would have been found first");
-//   S  stage (reads A, B' only): for every v != r,s the touching values
-//      δ'(r,v), δ'(s,v) of the POST-swap state from PRE-swap rows (R10b),
-//      4 lanes per v, 128-bit loads, dp4a; dA_v = a_vr - a_vs,
-//      dB_v = B'_vr - B'_vs; diagonal D_v = A_v . B'_v kept
-//      current; p, C, best, digest;
-//   U  update (writes Δ and B'): Δ in a padded "quad" layout so every thread
-//      updates 4 entries with one 128-bit load/store: disjoint entries
-//      Δ_uv += 2(dA_u-dA_v)(dB_u-dB_v) (R10), touching entries take the
-//      staged values, Δ_rs = -δ; B' rows/columns r,s exchanged (Eq.(3),
-//      P:90-94); the next window's addresses and thresholds are prepared.
+//   W  window: candidate k+o (o = window offset) is tested against Eq.(2)
+//       by thread NT-1-o, with its Δ address and threshold
+//      θ = -T ln r prepared off the critical path; a warp vote
+//      (__ballot_sync) + cross-warp min picks the first accepted candidate
+//      ("the swap which would have been found first").  Meanwhile the low
+//      threads apply the previous accept's B' row/column exchange (Eq.(3),
+//      P:90-94) and best_p copy.
+//   SU stage+update (reads A and the PRE-swap B'; writes Δ):
+//      touching entries: for every v != r,s the values δ''(r,v), δ''(s,v) of
+//        the post-swap state from pre-swap rows (R10b), 4 lanes per v, 128-bit
+//        loads and dp4a, written straight into Δ; diagonal D_v kept current;
+//      disjoint entries: Δ_uv += 2(dA_u-dA_v)(dB_u-dB_v) (R10) in a padded quad
+//        layout, one 128-bit load/store per 4 entries; every warp stages its own
+//        copy of dA_x = a_xr - a_xs, dB_x = B'_xr - B'_xs;
+//      p, C, best, digest; Δ_rs = -δ; next window's addresses and thresholds.
 // A window without an accepted candidate costs one barrier.
 //
-// Δ quad layout: NQ = ceil(n/4); row u keeps the
-// column quads j = floor((u+1)/4) .. NQ-1; quad g of the row-major sequence
-// holds entries (u, 4j..4j+3) at D[4g..4g+3]; entry (u,v) is at rowaddr[u]+v.
-// Slots with v <= u or v >= n are dead (never read for a decision).
-// Rows of A and B' have stride ld (a multiple of 16 elements).
+// Δ quad layout: NQ = ceil(n/4); row u keeps the column quads
+// j = floor((u+1)/4) .. NQ-1; quad g of the row-major sequence holds entries
+// (u, 4j..4j+3) at D[4g..4g+3]; entry (u,v) is at rowaddr[u]+v.  Slots with
+// v <= u or v >= n are dead (never read for a decision).  Rows of A and B'
+// have stride ld (a multiple of 16 elements).
 //
 // Citation keys: P:n = PAPER.md line n, R# = DESIGN.md readings.
 #pragma once
@@ -70,10 +70,8 @@ template <typename TA, typename TB>
 struct ChainSmem {
     TB* Bp;                            // n x ld, B'_ij = B_{p(i),p(j)}
     int32_t* D;                        // quad layout (shared or global memory)
-    typename Dab<TA, TB>::T* dAB;      // n4, staged (dA_x, dB_x)
+    typename Dab<TA, TB>::T* dAB;      // n4: staged (dA_x, dB_x)
     int32_t* Dg;                       // n, diagonal D_x = sum_k A_xk B'_xk
-    int32_t* Tr;                       // n4, staged δ'(r,v) + 2 D'_r
-    int32_t* Ts;                       // n4, staged δ'(s,v) + 2 D'_s
     uint16_t* p;                       // n
     uint16_t* best_p;                  // n
     int4* slots;                       // 2 * NW window slots (double buffered)
@@ -92,17 +90,25 @@ __host__ __device__ constexpr int quad_count(int n) {
     return c;
 }
 // row stride: a multiple of 16 elements; for 8-bit rows an odd multiple when it fits, so
-// that 8 rows read 16 bytes each at the same offset hit distinct banks (phase S).
+// that 8 rows read 16 bytes each at the same offset hit distinct banks (touching lanes).
 __host__ __device__ constexpr int row_stride(int n, bool odd16) {
     const int m = (n + 15) / 16;
     return 16 * ((odd16 && !(m & 1)) ? m + 1 : m);
 }
+// Work split of a group of NT threads for problem size n: warps [0, TW) compute the
+// touching entries (one lane per v); if the group has more warps, the others do the quads.
+__host__ __device__ constexpr int touch_warps(int n) { return (n + 31) / 32; }
+__host__ __device__ constexpr bool split_warps(int NT, int n) { return NT / 32 > touch_warps(n); }
+__host__ __device__ constexpr int quad_lo(int NT, int n) { return split_warps(NT, n) ? 32 * touch_warps(n) : 0; }
+__host__ __device__ constexpr int quads_per_thread(int NT, int n) {
+    return (quad_count(n) + (NT - quad_lo(NT, n)) - 1) / (NT - quad_lo(NT, n));
+}
+// thread of a group that owns the scalar state (p swap, C, best, digest)
+__host__ __device__ constexpr int scalar_tid(int NT, int n) {
+    return split_warps(NT, n) ? quad_lo(NT, n) : NT / 2;
+}
 
-// thread of a group that owns the scalar state (p swap, C, best, digest): lane 0 of
-// the third-to-last warp (idle in phase S when the group has spare warps)
-__host__ __device__ constexpr int scalar_tid(int NT) { return NT >= 96 ? NT - 96 : 0; }
-
-struct ChainScalars {  // meaningful in thread scalar_tid(NT) of the group
+struct ChainScalars {  // meaningful in thread scalar_tid(NT, n) of the group
     int64_t cost;
     int64_t best;
     uint64_t digest;
@@ -125,12 +131,13 @@ __device__ __forceinline__ int advance_cursor(int cur, int step, int M) {
 }
 
 // ---- touching dot products over 16-element blocks b = b0, b0+step, ... < nb
-// X_r += B'_v . a_r, X_s += B'_v . a_s, Y_r += A_v . b'_r, Y_s += A_v . b'_s
+// X_r += B'_v . a_r, X_s += B'_v . a_s, Y_r += A_v . b'_r, Y_s += A_v . b'_s,
+// Z_r += a_r . b'_s, Z_s += a_s . b'_r  (the last two do not depend on v)
 template <typename TA, typename TB>
 struct Dots {
     __device__ static void run(const TA* Av, const TB* Bv, const TA* Ar, const TA* As, const TB* Br,
                                const TB* Bs, int b0, int step, int nb, int& xr, int& xs, int& yr,
-                               int& ys) {
+                               int& ys, int& zr, int& zs) {
         for (int b = b0; b < nb; b += step)
             for (int k = 16 * b; k < 16 * b + 16; ++k) {
                 const int bv = Bv[k], av = Av[k];
@@ -138,6 +145,8 @@ struct Dots {
                 xs += bv * (int)As[k];
                 yr += av * (int)Br[k];
                 ys += av * (int)Bs[k];
+                zr += (int)Ar[k] * (int)Bs[k];
+                zs += (int)As[k] * (int)Br[k];
             }
     }
     __device__ static int dot(const TA* X, const TB* Y, int b0, int step, int nb) {
@@ -156,23 +165,27 @@ template <>
 struct Dots<uint8_t, uint8_t> {
     __device__ static void run(const uint8_t* Av, const uint8_t* Bv, const uint8_t* Ar,
                                const uint8_t* As, const uint8_t* Br, const uint8_t* Bs, int b0,
-                               int step, int nb, int& xr, int& xs, int& yr, int& ys) {
+                               int step, int nb, int& xr, int& xs, int& yr, int& ys, int& zr,
+                               int& zs) {
         const uint4* av = reinterpret_cast<const uint4*>(Av);
         const uint4* bv = reinterpret_cast<const uint4*>(Bv);
         const uint4* ar = reinterpret_cast<const uint4*>(Ar);
         const uint4* as = reinterpret_cast<const uint4*>(As);
         const uint4* br = reinterpret_cast<const uint4*>(Br);
         const uint4* bs = reinterpret_cast<const uint4*>(Bs);
-        uint32_t Xr = 0, Xs = 0, Yr = 0, Ys = 0;
+        uint32_t Xr = 0, Xs = 0, Yr = 0, Ys = 0, Zr = 0, Zs = 0;
 #pragma unroll 2
         for (int b = b0; b < nb; b += step) {
             const uint4 a = av[b], bb = bv[b];
-            Xr = dp16(bb, ar[b], Xr);
-            Xs = dp16(bb, as[b], Xs);
-            Yr = dp16(a, br[b], Yr);
-            Ys = dp16(a, bs[b], Ys);
+            const uint4 rA = ar[b], sA = as[b], rB = br[b], sB = bs[b];
+            Xr = dp16(bb, rA, Xr);
+            Xs = dp16(bb, sA, Xs);
+            Yr = dp16(a, rB, Yr);
+            Ys = dp16(a, sB, Ys);
+            Zr = dp16(rA, sB, Zr);
+            Zs = dp16(sA, rB, Zs);
         }
-        xr += (int)Xr; xs += (int)Xs; yr += (int)Yr; ys += (int)Ys;
+        xr += (int)Xr; xs += (int)Xs; yr += (int)Yr; ys += (int)Ys; zr += (int)Zr; zs += (int)Zs;
     }
     __device__ static int dot(const uint8_t* X, const uint8_t* Y, int b0, int step, int nb) {
         const uint4* x = reinterpret_cast<const uint4*>(X);
@@ -195,23 +208,27 @@ template <>
 struct Dots<uint8_t, uint16_t> {
     __device__ static void run(const uint8_t* Av, const uint16_t* Bv, const uint8_t* Ar,
                                const uint8_t* As, const uint16_t* Br, const uint16_t* Bs, int b0,
-                               int step, int nb, int& xr, int& xs, int& yr, int& ys) {
+                               int step, int nb, int& xr, int& xs, int& yr, int& ys, int& zr,
+                               int& zs) {
         const uint4* av = reinterpret_cast<const uint4*>(Av);
         const uint4* bv = reinterpret_cast<const uint4*>(Bv);
         const uint4* ar = reinterpret_cast<const uint4*>(Ar);
         const uint4* as = reinterpret_cast<const uint4*>(As);
         const uint4* br = reinterpret_cast<const uint4*>(Br);
         const uint4* bs = reinterpret_cast<const uint4*>(Bs);
-        uint32_t Xr = 0, Xs = 0, Yr = 0, Ys = 0;
+        uint32_t Xr = 0, Xs = 0, Yr = 0, Ys = 0, Zr = 0, Zs = 0;
         for (int b = b0; b < nb; b += step) {
             const uint4 a = av[b], b0w = bv[2 * b], b1w = bv[2 * b + 1];
             const uint4 r8 = ar[b], s8 = as[b];
+            const uint4 R0 = br[2 * b], R1 = br[2 * b + 1], S0 = bs[2 * b], S1 = bs[2 * b + 1];
             Xr = dp16w(r8, b0w, b1w, Xr);
             Xs = dp16w(s8, b0w, b1w, Xs);
-            Yr = dp16w(a, br[2 * b], br[2 * b + 1], Yr);
-            Ys = dp16w(a, bs[2 * b], bs[2 * b + 1], Ys);
+            Yr = dp16w(a, R0, R1, Yr);
+            Ys = dp16w(a, S0, S1, Ys);
+            Zr = dp16w(r8, S0, S1, Zr);
+            Zs = dp16w(s8, R0, R1, Zs);
         }
-        xr += (int)Xr; xs += (int)Xs; yr += (int)Yr; ys += (int)Ys;
+        xr += (int)Xr; xs += (int)Xs; yr += (int)Yr; ys += (int)Ys; zr += (int)Zr; zs += (int)Zs;
     }
     __device__ static int dot(const uint8_t* X, const uint16_t* Y, int b0, int step, int nb) {
         const uint4* x = reinterpret_cast<const uint4*>(X);
@@ -222,10 +239,16 @@ struct Dots<uint8_t, uint16_t> {
     }
 };
 
-constexpr int kTouchLanes = 4;   // lanes per touching v in phase S (lane = pl * 8 + v_local)
+// producer/consumer hand-off of the staged dA/dB between touching and quad warps
+__device__ __forceinline__ void stage_arrive(int id, int nthreads) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void stage_wait(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 
 // Optional phase timers (debug build with -DQAPSA_PHASE_TIMERS, tools/phase_times.py):
-// cycles spent by thread 0 of the group in W (accepting / non-accepting windows), S, U.
+// cycles spent by thread 0 of the group in W (accepting / non-accepting windows) and SU.
 #ifdef QAPSA_PHASE_TIMERS
 __device__ unsigned long long g_phase_cycles[8];
 #define PT_MARK(var) const long long var = clock64()
@@ -268,7 +291,7 @@ __device__ __forceinline__ void prepare_theta(Prep& pr, const Sched& sch, uint64
 
 // Runs iterations [k0, k_end) of one chain.  Returns the number of accepted
 // swaps (identical in every thread of the group).  QPT > 0: the thread's quads
-// (g = t + i NT, i < QPT) are fixed at compile time.
+// are fixed at compile time (g = t - quad_lo + i * (NT - quad_lo), i < QPT).
 template <typename TA, typename TB, int NT, int QPT>
 __device__ __forceinline__ uint64_t chain_run(const TA* __restrict__ A, const ChainSmem<TA, TB>& cs,
                                               const ChainTables tb, const int n, const int ld,
@@ -281,26 +304,29 @@ __device__ __forceinline__ uint64_t chain_run(const TA* __restrict__ A, const Ch
     using DB = Dab<TA, TB>;
     using DT = typename DB::T;
     constexpr int NW = NT / 32;
-    constexpr int TP = kTouchLanes;
     const int lane = t & 31, warp = t >> 5;
-    const int nb = ld >> 4;                    // 16-element blocks per row
-    // extra tasks of phase S go to the last warps (idle when NW > ceil(n/8) + 2)
-    const int w_dr = NW - 1, w_ds = NW >= 2 ? NW - 2 : 0;
-    const bool scalar_thread = t == scalar_tid(NT);
+    const int nb = ld >> 4;                        // 16-element blocks per row
+    const int off = NT - 1 - t;                    // this thread's window offset
+    const int TW = touch_warps(n);
+    const bool split = split_warps(NT, n);
+    const int qlo = quad_lo(NT, n), QT = NT - qlo;
+    const bool scalar_thread = t == scalar_tid(NT, n);
+    const int stage_bar = bar_id + 1;              // named barrier of the staging hand-off
 
     // quads owned by this thread (compile-time count when QPT > 0)
     uint32_t qd[QPT > 0 ? QPT : 1];
 #pragma unroll
     for (int i = 0; i < (QPT > 0 ? QPT : 0); ++i) {
-        const int g = t + i * NT;
-        qd[i] = g < nqt ? tb.qdesc[g] : 0xFFFFFFFFu;
+        const int g = t - qlo + i * QT;
+        qd[i] = (t >= qlo && g < nqt) ? tb.qdesc[g] : 0xFFFFFFFFu;
     }
 
     uint64_t k = k0, accepted = 0;
     int cur = (int)(k0 % (uint64_t)M);
     int W = wmax;
     int parity = 0;
-    bool streak = false;                       // previous window accepted nothing
+    bool streak = false;                           // previous window accepted nothing
+    int pend_r = -1, pend_s = -1;                  // B' exchange still to apply
     Prep pre;
     pre.k = ~0ull;
 
@@ -309,12 +335,39 @@ __device__ __forceinline__ uint64_t chain_run(const TA* __restrict__ A, const Ch
         const uint64_t remaining = k_end - k;
         const int Wl = (uint64_t)W < remaining ? W : (int)remaining;
 
-        // ---------------- W: window of candidates ----------------
+        // ---------------- W: window of candidates (+ deferred B' exchange) ----------------
+        if (pend_r >= 0) {
+            const int r = pend_r, s = pend_s;
+            for (int x = t; x < n; x += NT) {     // columns r,s of every other row
+                if (x == r || x == s) continue;
+                TB* row = cs.Bp + x * ld;
+                const TB br = row[r];
+                row[r] = row[s];
+                row[s] = br;
+            }
+            if (warp == 0) {                      // rows r,s, word-wise
+                constexpr int EPW = 4 / sizeof(TB);
+                constexpr uint32_t EMASK = sizeof(TB) == 1 ? 0xFFu : 0xFFFFu;
+                uint32_t* Rw = reinterpret_cast<uint32_t*>(cs.Bp + r * ld);
+                uint32_t* Sw = reinterpret_cast<uint32_t*>(cs.Bp + s * ld);
+                for (int w = lane; w < ld / EPW; w += 32) {
+                    uint32_t m = 0;
+                    if (r / EPW == w) m |= EMASK << (8 * sizeof(TB) * (r % EPW));
+                    if (s / EPW == w) m |= EMASK << (8 * sizeof(TB) * (s % EPW));
+                    const uint32_t a = Rw[w], b = Sw[w];
+                    Rw[w] = (b & ~m) | (a & m);   // rows exchange; (r,r),(r,s),(s,r),(s,s) keep
+                    Sw[w] = (a & ~m) | (b & m);   // their values (B' symmetric, zero diagonal)
+                }
+            }
+            if (cs.flags[0])
+                for (int x = t; x < n; x += NT) cs.best_p[x] = cs.p[x];
+            pend_r = -1;
+        }
         bool acc = false, near = false;
         int d = 0;
-        if (t < Wl) {
-            const uint64_t kk = k + (uint64_t)t;
-            if (pre.k != kk) prepare_addr(pre, n, tb.rowaddr, advance_cursor(cur, t, M), kk);
+        if (off < Wl) {
+            const uint64_t kk = k + (uint64_t)off;
+            if (pre.k != kk) prepare_addr(pre, n, tb.rowaddr, advance_cursor(cur, off, M), kk);
             d = cs.D[pre.addr];
             if (d <= 0) {
                 acc = true;                       // δ < 0, or δ = 0: exp(0) = 1 > r (R5)
@@ -331,27 +384,27 @@ __device__ __forceinline__ uint64_t chain_run(const TA* __restrict__ A, const Ch
         }
         int4* slots = cs.slots + parity * NW;
         const unsigned bal = __ballot_sync(0xffffffffu, acc);
-        if (bal) {
-            if (lane == __ffs(bal) - 1) slots[warp] = make_int4(t, d, pre.rs, 0);
+        if (bal) {                                // smallest offset = highest accepting lane
+            if (lane == 31 - __clz(bal)) slots[warp] = make_int4(off, d, pre.rs, 0);
         } else if (lane == 0) {
             slots[warp] = make_int4(INT_MAX, 0, 0, 0);
         }
         // in a run of windows without accepts, prepare the next window's addresses now
         const int Wn = min(2 * W, wmax);
-        if (streak && t < Wn && (uint64_t)(Wl + t) < remaining)
-            prepare_addr(pre, n, tb.rowaddr, advance_cursor(cur, Wl + t, M), k + (uint64_t)(Wl + t));
+        if (streak && off < Wn && (uint64_t)(Wl + off) < remaining)
+            prepare_addr(pre, n, tb.rowaddr, advance_cursor(cur, Wl + off, M), k + (uint64_t)(Wl + off));
         group_sync(bar_id, NT);
         PT_MARK(pt1);
         const int tv = lane < NW ? slots[lane].x : INT_MAX;
         const int j = __reduce_min_sync(0xffffffffu, tv);
         parity ^= 1;
         const int consumed = (j == INT_MAX) ? Wl : j + 1;
-        if (near && t < consumed) {               // R16: count / log near ties of consumed iterations
+        if (near && off < consumed) {             // R16: count / log near ties of consumed iterations
             atomicAdd(&cs.flags[1], 1);
             if (sink.count) {
                 const unsigned int i = atomicAdd(sink.count, 1u);
                 if ((int)i < sink.cap) {
-                    sink.ks[i] = (unsigned long long)(k + (uint64_t)t);
+                    sink.ks[i] = (unsigned long long)(k + (uint64_t)off);
                     sink.dec[i] = acc ? 1 : 0;
                 }
             }
@@ -366,61 +419,91 @@ __device__ __forceinline__ uint64_t chain_run(const TA* __restrict__ A, const Ch
             continue;
         }
         streak = false;
-        const int4 win = slots[(j >> 5)];         // (t, δ, r<<16|s) of the first accepted candidate
+        const int4 win = slots[(NT - 1 - j) >> 5];   // (offset, δ, r<<16|s) of the first accept
         const int dw = win.y, r = win.z >> 16, s = win.z & 0xFFFF;
         const uint64_t kacc = k + (uint64_t)j;
+        const int Wnext = max(64, min(wmax, round_up32(8 * (j + 1))));
 
-        // ---------------- S: stage touching values, dA/dB, diagonal (reads A, B') ----------------
+        // ---------------- SU: touching values, disjoint quads, scalars (B' read-only) ----------------
         {
             const TA* Ar = A + r * ld;
             const TA* As = A + s * ld;
             const TB* Br = cs.Bp + r * ld;
             const TB* Bs = cs.Bp + s * ld;
             const int ars = Ar[s], brs = Br[s];
-            const int vl = lane & 7, pl = lane >> 3;
-            for (int vb = 0; vb < n; vb += 8 * NW) {
-                const int v = vb + 8 * warp + vl;
-                const bool act = v < n && v != r && v != s;
-                int arv = 0, asv = 0, brv = 0, bsv = 0, dgv = 0;
-                if (act && pl == 0) {
-                    arv = Ar[v]; asv = As[v]; brv = Br[v]; bsv = Bs[v]; dgv = cs.Dg[v];
-                }
-                int xr = 0, xs = 0, yr = 0, ys = 0;
-                if (act)
-                    Dots<TA, TB>::run(A + v * ld, cs.Bp + v * ld, Ar, As, Br, Bs, pl, TP, nb, xr, xs,
-                                      yr, ys);
-#pragma unroll
-                for (int o = 8; o < 32; o <<= 1) {
-                    xr += __shfl_xor_sync(0xffffffffu, xr, o);
-                    xs += __shfl_xor_sync(0xffffffffu, xs, o);
-                    yr += __shfl_xor_sync(0xffffffffu, yr, o);
-                    ys += __shfl_xor_sync(0xffffffffu, ys, o);
-                }
-                if (act && pl == 0) {
-                    const int da = arv - asv;             // dA_v = a_vr - a_vs
-                    const int db = brv - bsv;             // dB_v = B'_vr - B'_vs (pre-swap)
-                    cs.dAB[v] = DB::pack(da, db);
-                    const int dv = dgv - da * db;         // D''_v = D_v - dA_v dB_v
-                    cs.Dg[v] = dv;
-                    // R10b: δ''(r,v) + 2D''_r and δ''(s,v) + 2D''_s from pre-swap rows
-                    cs.Tr[v] = 2 * (xr + ars * db + ys - da * brs - dv + 2 * arv * bsv);
-                    cs.Ts[v] = 2 * (xs - ars * db + yr + da * brs - dv + 2 * asv * brv);
+            // address and threshold of this thread's candidate in the next window
+            if (off < Wnext && kacc + 1 + (uint64_t)off < k_end) {
+                prepare_addr(pre, n, tb.rowaddr, advance_cursor(cur, j + 1 + off, M),
+                             kacc + 1 + (uint64_t)off);
+                prepare_theta(pre, sch, seed, chain);
+            }
+            // -- touching entries (rows / columns r and s): one lane per v --
+            if (!split || warp < TW) {
+                const int vmin = r != 0 ? 0 : (s != 1 ? 1 : 2);
+                for (int vb = 0; vb < n; vb += 32 * (split ? TW : NW)) {
+                    const int v = vb + 32 * warp + lane;
+                    const bool act = v < n && v != r && v != s;
+                    int arv = 0, asv = 0, brv = 0, bsv = 0, da = 0, db = 0;
+                    if (act) {                        // staging, handed to the quad warps
+                        arv = Ar[v]; asv = As[v]; brv = Br[v]; bsv = Bs[v];
+                        da = arv - asv;               // dA_v = a_vr - a_vs
+                        db = brv - bsv;               // dB_v = B'_vr - B'_vs (pre-swap)
+                        cs.dAB[v] = DB::pack(da, db);
+                    }
+                    if (split && vb == 0) stage_arrive(stage_bar, NT);
+                    if (act) {
+                        int xr = 0, xs = 0, yr = 0, ys = 0, zr = 0, zs = 0;
+                        Dots<TA, TB>::run(A + v * ld, cs.Bp + v * ld, Ar, As, Br, Bs, 0, 1, nb, xr, xs,
+                                          yr, ys, zr, zs);
+                        const int Dr = zr + ars * brs;        // D''_r = a_r.b'_s + a_rs B'_rs
+                        const int Ds = zs + ars * brs;        // D''_s = a_s.b'_r + a_rs B'_rs
+                        const int dv = cs.Dg[v] - da * db;    // D''_v = D_v - dA_v dB_v
+                        cs.Dg[v] = dv;
+                        // R10b: δ''(r,v) and δ''(s,v) from pre-swap rows
+                        cs.D[v > r ? tb.rowaddr[r] + v : tb.rowaddr[v] + r] =
+                            2 * (xr + ars * db + ys - da * brs - Dr - dv + 2 * arv * bsv);
+                        cs.D[v > s ? tb.rowaddr[s] + v : tb.rowaddr[v] + s] =
+                            2 * (xs - ars * db + yr + da * brs - Ds - dv + 2 * asv * brv);
+                        if (v == vmin) {
+                            cs.Dg[r] = Dr;
+                            cs.Dg[s] = Ds;
+                        }
+                    }
                 }
             }
-            if (warp == w_dr || warp == w_ds) {
-                // D''_r = sum_k a_rk B'_sk + a_rs B'_sr,  D''_s = sum_k a_sk B'_rk + a_sr B'_rs
-                int dr = 0, ds = 0;
-                if (warp == w_dr) dr = Dots<TA, TB>::dot(Ar, Bs, lane, 32, nb);
-                if (warp == w_ds) ds = Dots<TA, TB>::dot(As, Br, lane, 32, nb);
+            // -- disjoint entries: every quad of a row u != r,s --
+            if (!split || warp >= TW) {
+                if (split) stage_wait(stage_bar, NT);
+                else group_sync(stage_bar, NT);
+                const DT* stg = cs.dAB;
+                auto quad = [&](const uint32_t desc, const int g) {
+                    const int u = desc & 511, v0 = (desc >> 9) << 2;
+                    if (u == r || u == s) return;     // rows r, s: touching lanes
+                    const int4 d4 = *reinterpret_cast<const int4*>(cs.D + 4 * g);
+                    const DT pu = stg[u];
+                    DT pv[4];
+                    DB::load4(stg, v0, pv);
+                    const int4 nv = make_int4(d4.x + DB::rank(pu, pv[0]), d4.y + DB::rank(pu, pv[1]),
+                                              d4.z + DB::rank(pu, pv[2]), d4.w + DB::rank(pu, pv[3]));
+                    const unsigned er = (unsigned)(r - v0), es = (unsigned)(s - v0);
+                    if (er < 4u || es < 4u) {         // columns r/s belong to the touching lanes
+                        if (er != 0u && es != 0u) cs.D[4 * g + 0] = nv.x;
+                        if (er != 1u && es != 1u) cs.D[4 * g + 1] = nv.y;
+                        if (er != 2u && es != 2u) cs.D[4 * g + 2] = nv.z;
+                        if (er != 3u && es != 3u) cs.D[4 * g + 3] = nv.w;
+                    } else {
+                        *reinterpret_cast<int4*>(cs.D + 4 * g) = nv;
+                    }
+                };
+                if (QPT > 0) {
 #pragma unroll
-                for (int o = 16; o; o >>= 1) {
-                    dr += __shfl_xor_sync(0xffffffffu, dr, o);
-                    ds += __shfl_xor_sync(0xffffffffu, ds, o);
+                    for (int i = 0; i < (QPT > 0 ? QPT : 1); ++i)
+                        if (qd[i] != 0xFFFFFFFFu) quad(qd[i], t - qlo + i * QT);
+                } else {
+                    for (int g = t - qlo; g < nqt; g += QT) quad(tb.qdesc[g], g);
                 }
-                if (lane == 0 && warp == w_dr) cs.Dg[r] = dr + ars * brs;
-                if (lane == 0 && warp == w_ds) cs.Dg[s] = ds + ars * brs;
             }
-            if (scalar_thread) {                  // scalar state: p, C, best, digest
+            if (scalar_thread) {                  // scalar state: p, C, best, digest, Δ_rs
                 const uint16_t pr = cs.p[r];
                 cs.p[r] = cs.p[s];
                 cs.p[s] = pr;
@@ -429,81 +512,19 @@ __device__ __forceinline__ uint64_t chain_run(const TA* __restrict__ A, const Ch
                 if (improved) io.best = io.cost;
                 cs.flags[0] = improved;
                 io.digest = digest_step(io.digest, kacc, r, s);
+                cs.D[tb.rowaddr[r] + s] = -dw;    // swapping back restores C
+                if (n < 3) {                      // no touching lane: diagonal of rows r,s here
+                    cs.Dg[r] = Dots<TA, TB>::dot(Ar, Bs, 0, 1, nb) + ars * brs;
+                    cs.Dg[s] = Dots<TA, TB>::dot(As, Br, 0, 1, nb) + ars * brs;
+                }
             }
         }
-        group_sync(bar_id, NT);
-        PT_MARK(pt2);
-
-        // ---------------- U: Δ update (quads), B' exchange, next window ----------------
-        const int Wnext = max(64, min(wmax, round_up32(8 * (j + 1))));
-        {
-            // address and threshold of this thread's candidate in the next window
-            // (state independent; issued first so its latency overlaps the quad updates)
-            if (t < Wnext && kacc + 1 + (uint64_t)t < k_end) {
-                prepare_addr(pre, n, tb.rowaddr, advance_cursor(cur, j + 1 + t, M), kacc + 1 + (uint64_t)t);
-                prepare_theta(pre, sch, seed, chain);
-            }
-            const int Dr2 = 2 * cs.Dg[r], Ds2 = 2 * cs.Dg[s];
-            auto quad = [&](const uint32_t desc, const int g) {
-                const int u = desc & 511, v0 = (desc >> 9) << 2;
-                const int4 d4 = *reinterpret_cast<const int4*>(cs.D + 4 * g);
-                const DT pu = cs.dAB[u];
-                DT pv[4];
-                DB::load4(cs.dAB, v0, pv);
-                int4 nv = make_int4(d4.x + DB::rank(pu, pv[0]), d4.y + DB::rank(pu, pv[1]),
-                                    d4.z + DB::rank(pu, pv[2]), d4.w + DB::rank(pu, pv[3]));
-                const int er = r - v0, es = s - v0;
-                const bool rowr = u == r, rows = u == s;
-                if (rowr | rows) {                  // rows r, s: all touching
-                    const int4 t4 = *reinterpret_cast<const int4*>((rowr ? cs.Tr : cs.Ts) + v0);
-                    const int D2 = rowr ? Dr2 : Ds2;
-                    nv = make_int4(t4.x - D2, t4.y - D2, t4.z - D2, t4.w - D2);
-                }
-                *reinterpret_cast<int4*>(cs.D + 4 * g) = nv;
-                if (rowr && (unsigned)es < 4u) cs.D[4 * g + es] = -dw;   // swapping back restores C
-                if (!(rowr | rows)) {
-                    if ((unsigned)er < 4u) cs.D[4 * g + er] = cs.Tr[u] - Dr2;   // column r: δ''(u,r)
-                    if ((unsigned)es < 4u) cs.D[4 * g + es] = cs.Ts[u] - Ds2;   // column s: δ''(u,s)
-                }
-            };
-            if (QPT > 0) {
-#pragma unroll
-                for (int i = 0; i < (QPT > 0 ? QPT : 1); ++i)
-                    if (qd[i] != 0xFFFFFFFFu) quad(qd[i], t + i * NT);
-            } else {
-                for (int g = t; g < nqt; g += NT) quad(tb.qdesc[g], g);
-            }
-            // B' exchange: columns r,s of every other row, then rows r,s (word-wise)
-            for (int x = t; x < n; x += NT) {
-                if (x == r || x == s) continue;
-                TB* row = cs.Bp + x * ld;
-                const TB br = row[r];
-                row[r] = row[s];
-                row[s] = br;
-            }
-            if (warp == w_dr) {
-                constexpr int EPW = 4 / sizeof(TB);   // elements per 32-bit word
-                constexpr uint32_t EMASK = sizeof(TB) == 1 ? 0xFFu : 0xFFFFu;
-                const int nwords = ld / EPW;
-                uint32_t* Rw = reinterpret_cast<uint32_t*>(cs.Bp + r * ld);
-                uint32_t* Sw = reinterpret_cast<uint32_t*>(cs.Bp + s * ld);
-                for (int w = lane; w < nwords; w += 32) {
-                    uint32_t m = 0;
-                    if (r / EPW == w) m |= EMASK << (8 * sizeof(TB) * (r % EPW));
-                    if (s / EPW == w) m |= EMASK << (8 * sizeof(TB) * (s % EPW));
-                    const uint32_t a = Rw[w], b = Sw[w];
-                    Rw[w] = (b & ~m) | (a & m);   // rows exchange; (r,r),(r,s),(s,r),(s,s) keep
-                    Sw[w] = (a & ~m) | (b & m);   // their values (B' symmetric, zero diagonal)
-                }
-            }
-            if (cs.flags[0])
-                for (int x = t; x < n; x += NT) cs.best_p[x] = cs.p[x];
-        }
+        pend_r = r;
+        pend_s = s;
         group_sync(bar_id, NT);
         PT_MARK(pt3);
         PT_ADD(0, pt0, pt1);
-        PT_ADD(2, pt1, pt2);
-        PT_ADD(3, pt2, pt3);
+        PT_ADD(2, pt1, pt3);
         PT_ADD(4, 0, 1);
 
         ++accepted;
@@ -511,6 +532,10 @@ __device__ __forceinline__ uint64_t chain_run(const TA* __restrict__ A, const Ch
         cur = advance_cursor(cur, j + 1, M);
         W = Wnext;
     }
+    // the B' exchange of the last accept is not needed (B' is rebuilt from p at the next
+    // launch); its best_p copy is
+    if (pend_r >= 0 && cs.flags[0])
+        for (int x = t; x < n; x += NT) cs.best_p[x] = cs.p[x];
     return accepted;
 }
 

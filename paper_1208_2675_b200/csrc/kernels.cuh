@@ -32,7 +32,7 @@ struct ChainResult {              // mirrors qap_chain_result
 
 // ---------------- shared-memory layout of one chain group ----------------
 struct GroupLayout {
-    int bp, d, dab, dg, tr, ts, p, bestp, slots, flags, bytes;
+    int bp, d, dab, dg, p, bestp, slots, flags, bytes;
 };
 __host__ __device__ inline int align16(int x) { return (x + 15) & ~15; }
 // dab_bytes: 4 when A and B are both 8-bit (packed int16 pair), else 8
@@ -46,8 +46,6 @@ __host__ __device__ inline GroupLayout group_layout(int n, int ld, int nqt, int 
     L.d = o;     o = align16(o + (d_in_smem ? nqt * 16 : 0));
     L.dab = o;   o = align16(o + n4 * dab_bytes);
     L.dg = o;    o = align16(o + n * 4);
-    L.tr = o;    o = align16(o + n4 * 4);
-    L.ts = o;    o = align16(o + n4 * 4);
     L.p = o;     o = align16(o + n * 2);
     L.bestp = o; o = align16(o + n * 2);
     L.slots = o; o = align16(o + 2 * nw * 16);
@@ -64,8 +62,6 @@ __device__ inline ChainSmem<TA, TB> group_view(unsigned char* base, const GroupL
     cs.D = d_global ? d_global : reinterpret_cast<int32_t*>(base + L.d);
     cs.dAB = reinterpret_cast<typename Dab<TA, TB>::T*>(base + L.dab);
     cs.Dg = reinterpret_cast<int32_t*>(base + L.dg);
-    cs.Tr = reinterpret_cast<int32_t*>(base + L.tr);
-    cs.Ts = reinterpret_cast<int32_t*>(base + L.ts);
     cs.p = reinterpret_cast<uint16_t*>(base + L.p);
     cs.best_p = reinterpret_cast<uint16_t*>(base + L.bestp);
     cs.slots = reinterpret_cast<int4*>(base + L.slots);
@@ -258,7 +254,7 @@ __global__ void __launch_bounds__(NT, 1) k_sa_chain(const ChainArgs a) {
     __syncthreads();
 
     const NearSink sink{a.near_count, a.near_k, a.near_dec, a.near_cap};
-    constexpr int QPT = NFIX ? (quad_count(NFIX) + NT - 1) / NT : 0;
+    constexpr int QPT = NFIX ? quads_per_thread(NT, NFIX) : 0;
     const uint64_t acc = chain_run<TA, TB, NT, QPT>(As, cs, tb, n, ld, M, nqt, a.k0, a.k_end, a.sch,
                                                     a.seed, 0u, 0, t, a.wmax, io, sink);
 
@@ -267,7 +263,7 @@ __global__ void __launch_bounds__(NT, 1) k_sa_chain(const ChainArgs a) {
         a.best_p[i] = cs.best_p[i];
     }
     if (D_SMEM) copy_words(a.D, cs.D, nqt * 16, t, NT);
-    if (t == scalar_tid(NT)) {
+    if (t == scalar_tid(NT, n)) {
         a.st->cost = io.cost;
         a.st->best_cost = io.best;
         a.st->digest = io.digest;
@@ -305,7 +301,7 @@ __global__ void __launch_bounds__(1024, 1) k_ensemble(const EnsArgs a) {
     uint16_t* qdesc = reinterpret_cast<uint16_t*>(smem + a_bytes + align16(n * 4));
     const GroupLayout L = group_layout(n, ld, nqt, sizeof(TB), NT / 32, true,
                                        sizeof(typename Dab<TA, TB>::T));
-    const int g = threadIdx.x / NT, t = threadIdx.x % NT, bar = 1 + g;
+    const int g = threadIdx.x / NT, t = threadIdx.x % NT, bar = 1 + 2 * g;  // +1: staging hand-off
     ChainSmem<TA, TB> cs =
         group_view<TA, TB>(smem + cta_prefix_bytes(n, ld, sizeof(TA), nqt) + g * L.bytes, L, nullptr);
     const ChainTables tb{rowaddr, qdesc};
@@ -346,12 +342,12 @@ __global__ void __launch_bounds__(1024, 1) k_ensemble(const EnsArgs a) {
         io.best = io.cost;
         group_sync(bar, NT);
         const NearSink sink{nullptr, nullptr, nullptr, 0};
-        constexpr int QPT = NFIX ? (quad_count(NFIX) + NT - 1) / NT : 0;
+        constexpr int QPT = NFIX ? quads_per_thread(NT, NFIX) : 0;
         const uint64_t acc = chain_run<TA, TB, NT, QPT>(As, cs, tb, n, ld, M, nqt, 0ull, a.iters, a.sch,
                                                    a.seed, a.chain_begin + (unsigned)ci, bar, t,
                                                    a.wmax, io, sink);
         for (int i = t; i < n; i += NT) a.best_perms[(size_t)ci * n + i] = cs.best_p[i];
-        if (t == scalar_tid(NT)) {
+        if (t == scalar_tid(NT, n)) {
             ChainResult r;
             r.cost = io.cost;
             r.best_cost = io.best;

@@ -356,9 +356,12 @@ static cudaError_t launch_generic(qap_ctx* c, const ChainArgs& a, bool ds, int s
 }
 
 // Threads of the single-chain CTA: enough for 4 lanes per touching v and <= 3 quads per thread.
+// Threads of the single-chain CTA: touching warps (8 v each) plus quad warps with
+// <= 3 quads per thread, rounded to a power of two.
 static int auto_threads(const qap_ctx* c) {
+    const int need = 32 * touch_warps(c->n) + (c->nqt + 2) / 3;
     int nt = 64;
-    while (nt < 1024 && (nt < 4 * c->n || 3 * nt < c->nqt)) nt *= 2;
+    while (nt < 1024 && nt < need) nt *= 2;
     return nt;
 }
 
@@ -368,9 +371,9 @@ static cudaError_t launch_chain(qap_ctx* c, const ChainArgs& a, int threads, boo
                                 bool ds, int smem) {
     if (!explicit_threads) {
         if (c->ta == 1 && c->tb == 1 && ds) {
-            if (c->n == 12 && threads == 64) return launch_chain_t<uint8_t, uint8_t, 64, true, 12>(c, a, smem);
-            if (c->n == 50 && threads == 256) return launch_chain_t<uint8_t, uint8_t, 256, true, 50>(c, a, smem);
-            if (c->n == 100 && threads == 512) return launch_chain_t<uint8_t, uint8_t, 512, true, 100>(c, a, smem);
+            if (c->n == 12 && threads == 128) return launch_chain_t<uint8_t, uint8_t, 128, true, 12>(c, a, smem);
+            if (c->n == 50 && threads == 512) return launch_chain_t<uint8_t, uint8_t, 512, true, 50>(c, a, smem);
+            if (c->n == 100 && threads == 1024) return launch_chain_t<uint8_t, uint8_t, 1024, true, 100>(c, a, smem);
         }
         if (c->ta == 1 && c->tb == 2 && !ds && c->n == 256 && threads == 1024)
             return launch_chain_t<uint8_t, uint16_t, 1024, false, 256>(c, a, smem);
@@ -573,7 +576,8 @@ qap_status qap_ensemble_run(qap_ctx* c, uint32_t chain_begin, uint32_t chain_cou
     const int nt = (c->ta == 1 && c->tb == 1) ? c->ens_group : 128;
     const GroupLayout L = group_layout(n, c->ld, c->nqt, c->tb, nt / 32, true, dab_bytes(c));
     const int a_bytes = cta_prefix_bytes(n, c->ld, c->ta, c->nqt);
-    int groups = std::min((c->smem_optin - a_bytes) / L.bytes, 1024 / nt);
+    // each group uses 2 of the 16 hardware named barriers (ids 1+2g, 2+2g; id 0 is the CTA's)
+    int groups = std::min(std::min((c->smem_optin - a_bytes) / L.bytes, 1024 / nt), 7);
     if (groups < 1) return fail(c, QAP_E_UNSUPPORTED, "one ensemble chain does not fit on chip");
     const int smem = a_bytes + groups * L.bytes;
     CU(cudaSetDevice(c->dev));
