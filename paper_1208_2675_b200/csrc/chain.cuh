@@ -250,11 +250,24 @@ __device__ __forceinline__ void stage_wait(int id, int nthreads) {
 // Optional phase timers (debug build with -DQAPSA_PHASE_TIMERS, tools/phase_times.py):
 // cycles spent by thread 0 of the group in W (accepting / non-accepting windows) and SU.
 #ifdef QAPSA_PHASE_TIMERS
-__device__ unsigned long long g_phase_cycles[8];
+__device__ unsigned long long g_phase_cycles[16];
+#define PT_COUNT(slot) atomicAdd(&g_phase_cycles[slot], 1ull)
+// clock read that waits for `dep` (a shared-memory value read after a barrier): with
+// BAR.SYNC.DEFER_BLOCKING a plain clock read would be issued before the barrier releases
+__device__ __forceinline__ long long clock_after(int dep) {
+    long long c;
+    asm volatile("{\n\t.reg .b32 d;\n\tmov.b32 d, %1;\n\tmov.u64 %0, %%clock64;\n\t}" : "=l"(c) : "r"(dep) : "memory");
+    return c;
+}
 #define PT_MARK(var) const long long var = clock64()
+#define PT_MARKD(var, dep) const long long var = clock_after(dep)
 #define PT_ADD(slot, a, b) if (t == 0) atomicAdd(&g_phase_cycles[slot], (unsigned long long)((b) - (a)))
+#define PT_ADDT(tid, slot, a) if (t == (tid)) atomicAdd(&g_phase_cycles[slot], (unsigned long long)(clock64() - (a)))
 #else
+#define PT_ADDT(tid, slot, a)
 #define PT_MARK(var)
+#define PT_COUNT(slot)
+#define PT_MARKD(var, dep)
 #define PT_ADD(slot, a, b)
 #endif
 
@@ -306,7 +319,7 @@ __device__ __forceinline__ uint64_t chain_run(const TA* __restrict__ A, const Ch
     constexpr int NW = NT / 32;
     const int lane = t & 31, warp = t >> 5;
     const int nb = ld >> 4;                        // 16-element blocks per row
-    const int off = NT - 1 - t;                    // this thread's window offset
+    const int off = NT - 1 - t;                    // this thread's window offset (quad warps first)
     const int TW = touch_warps(n);
     const bool split = split_warps(NT, n);
     const int qlo = quad_lo(NT, n), QT = NT - qlo;
@@ -326,19 +339,26 @@ __device__ __forceinline__ uint64_t chain_run(const TA* __restrict__ A, const Ch
     int W = wmax;
     int parity = 0;
     bool streak = false;                           // previous window accepted nothing
+    float rejT = 38.5f * temp32(sch, k0);          // certain-reject bound of the current window
     int pend_r = -1, pend_s = -1;                  // B' exchange still to apply
     Prep pre;
     pre.k = ~0ull;
+#ifdef QAPSA_PHASE_TIMERS
+    long long su_start = 0;
+#endif
 
     while (k < k_end) {
-        PT_MARK(pt0);
+#ifdef QAPSA_PHASE_TIMERS
+        PT_MARKD(pt0, cs.flags[3]);
+        if (!streak && k != k0) PT_ADD(2, su_start, pt0);   // SU of the previous accept, barrier included
+#endif
         const uint64_t remaining = k_end - k;
         const int Wl = (uint64_t)W < remaining ? W : (int)remaining;
 
         // ---------------- W: window of candidates (+ deferred B' exchange) ----------------
         if (pend_r >= 0) {
             const int r = pend_r, s = pend_s;
-            for (int x = t; x < n; x += NT) {     // columns r,s of every other row
+            for (int x = t; x < n; x += NT) {     // columns r,s of every other row (low threads)
                 if (x == r || x == s) continue;
                 TB* row = cs.Bp + x * ld;
                 const TB br = row[r];
@@ -362,26 +382,36 @@ __device__ __forceinline__ uint64_t chain_run(const TA* __restrict__ A, const Ch
             if (cs.flags[0])
                 for (int x = t; x < n; x += NT) cs.best_p[x] = cs.p[x];
             pend_r = -1;
+#ifdef QAPSA_PHASE_TIMERS
+            if (t == NT - 1) atomicAdd(&g_phase_cycles[7], (unsigned long long)(clock_after(cs.Bp[s]) - pt0));
+#endif
         }
         bool acc = false, near = false;
         int d = 0;
         if (off < Wl) {
             const uint64_t kk = k + (uint64_t)off;
-            if (pre.k != kk) prepare_addr(pre, n, tb.rowaddr, advance_cursor(cur, off, M), kk);
+#ifdef QAPSA_PHASE_TIMERS
+            if (t == 0 && !streak) atomicAdd(&g_phase_cycles[11], (unsigned long long)(clock_after((int)pre.k + Wl) - pt0));
+#endif
+            if (pre.k != kk) { PT_COUNT(8); prepare_addr(pre, n, tb.rowaddr, advance_cursor(cur, off, M), kk); }
             d = cs.D[pre.addr];
             if (d <= 0) {
                 acc = true;                       // δ < 0, or δ = 0: exp(0) = 1 > r (R5)
-            } else if ((float)d <= 38.5f * temp32(sch, k)) {
+            } else if ((float)d <= rejT) {
                 // else certain reject: δ > 38.5 T32(k) >= 38.4 T_kk => exp(-δ/T) < 2^-54 <= r
-                if (pre.th < 0.0f) prepare_theta(pre, sch, seed, chain);
+                if (pre.th < 0.0f) { PT_COUNT(9); prepare_theta(pre, sch, seed, chain); }
                 const float df = (float)d;
                 if (df < pre.th - pre.m) {
                     acc = true;                   // clearly below θ
                 } else if (!(df > pre.th + pre.m)) {   // inside the margin: exact double test (R16)
+                    PT_COUNT(10);
                     acc = metropolis(d, temperature(sch, kk), uniform_r(seed, kk, chain), &near);
                 }
             }
         }
+#ifdef QAPSA_PHASE_TIMERS
+        if (t == NT - 1 && !streak) atomicAdd(&g_phase_cycles[6], (unsigned long long)(clock_after(d + (int)acc) - pt0));
+#endif
         int4* slots = cs.slots + parity * NW;
         const unsigned bal = __ballot_sync(0xffffffffu, acc);
         if (bal) {                                // smallest offset = highest accepting lane
@@ -394,8 +424,8 @@ __device__ __forceinline__ uint64_t chain_run(const TA* __restrict__ A, const Ch
         if (streak && off < Wn && (uint64_t)(Wl + off) < remaining)
             prepare_addr(pre, n, tb.rowaddr, advance_cursor(cur, Wl + off, M), k + (uint64_t)(Wl + off));
         group_sync(bar_id, NT);
-        PT_MARK(pt1);
         const int tv = lane < NW ? slots[lane].x : INT_MAX;
+        PT_MARKD(pt1, tv);
         const int j = __reduce_min_sync(0xffffffffu, tv);
         parity ^= 1;
         const int consumed = (j == INT_MAX) ? Wl : j + 1;
@@ -415,12 +445,16 @@ __device__ __forceinline__ uint64_t chain_run(const TA* __restrict__ A, const Ch
             k += (uint64_t)consumed;
             cur = advance_cursor(cur, consumed, M);
             W = Wn;
+            rejT = 38.5f * temp32(sch, k);
             streak = true;
             continue;
         }
         streak = false;
         const int4 win = slots[(NT - 1 - j) >> 5];   // (offset, δ, r<<16|s) of the first accept
         const int dw = win.y, r = win.z >> 16, s = win.z & 0xFFFF;
+#ifdef QAPSA_PHASE_TIMERS
+
+#endif
         const uint64_t kacc = k + (uint64_t)j;
         const int Wnext = max(64, min(wmax, round_up32(8 * (j + 1))));
 
@@ -431,12 +465,6 @@ __device__ __forceinline__ uint64_t chain_run(const TA* __restrict__ A, const Ch
             const TB* Br = cs.Bp + r * ld;
             const TB* Bs = cs.Bp + s * ld;
             const int ars = Ar[s], brs = Br[s];
-            // address and threshold of this thread's candidate in the next window
-            if (off < Wnext && kacc + 1 + (uint64_t)off < k_end) {
-                prepare_addr(pre, n, tb.rowaddr, advance_cursor(cur, j + 1 + off, M),
-                             kacc + 1 + (uint64_t)off);
-                prepare_theta(pre, sch, seed, chain);
-            }
             // -- touching entries (rows / columns r and s): one lane per v --
             if (!split || warp < TW) {
                 const int vmin = r != 0 ? 0 : (s != 1 ? 1 : 2);
@@ -449,12 +477,18 @@ __device__ __forceinline__ uint64_t chain_run(const TA* __restrict__ A, const Ch
                         da = arv - asv;               // dA_v = a_vr - a_vs
                         db = brv - bsv;               // dB_v = B'_vr - B'_vs (pre-swap)
                         cs.dAB[v] = DB::pack(da, db);
+#ifdef QAPSA_PHASE_TIMERS
+
+#endif
                     }
                     if (split && vb == 0) stage_arrive(stage_bar, NT);
                     if (act) {
                         int xr = 0, xs = 0, yr = 0, ys = 0, zr = 0, zs = 0;
                         Dots<TA, TB>::run(A + v * ld, cs.Bp + v * ld, Ar, As, Br, Bs, 0, 1, nb, xr, xs,
                                           yr, ys, zr, zs);
+#ifdef QAPSA_PHASE_TIMERS
+                        if (t == 0) atomicAdd(&g_phase_cycles[12], (unsigned long long)(clock_after(xr + ys + zr) - pt1));
+#endif
                         const int Dr = zr + ars * brs;        // D''_r = a_r.b'_s + a_rs B'_rs
                         const int Ds = zs + ars * brs;        // D''_s = a_s.b'_r + a_rs B'_rs
                         const int dv = cs.Dg[v] - da * db;    // D''_v = D_v - dA_v dB_v
@@ -475,6 +509,9 @@ __device__ __forceinline__ uint64_t chain_run(const TA* __restrict__ A, const Ch
             if (!split || warp >= TW) {
                 if (split) stage_wait(stage_bar, NT);
                 else group_sync(stage_bar, NT);
+#ifdef QAPSA_PHASE_TIMERS
+                if (t == qlo) atomicAdd(&g_phase_cycles[3], (unsigned long long)(clock_after(cs.flags[3]) - pt1));
+#endif
                 const DT* stg = cs.dAB;
                 auto quad = [&](const uint32_t desc, const int g) {
                     const int u = desc & 511, v0 = (desc >> 9) << 2;
@@ -496,13 +533,57 @@ __device__ __forceinline__ uint64_t chain_run(const TA* __restrict__ A, const Ch
                     }
                 };
                 if (QPT > 0) {
+                    // all loads of this thread's quads first, then the arithmetic and stores
+                    constexpr int QP = QPT > 0 ? QPT : 1;
+                    int4 d4[QP];
+                    DT pu[QP], pv[QP][4];
+                    int gq[QP], v0q[QP];
+                    bool stq[QP];
 #pragma unroll
-                    for (int i = 0; i < (QPT > 0 ? QPT : 1); ++i)
-                        if (qd[i] != 0xFFFFFFFFu) quad(qd[i], t - qlo + i * QT);
+                    for (int i = 0; i < QP; ++i) {
+                        const uint32_t desc = qd[i];
+                        const bool valid = desc != 0xFFFFFFFFu;
+                        const int u = valid ? (int)(desc & 511) : 0;
+                        v0q[i] = valid ? (int)((desc >> 9) << 2) : 0;
+                        gq[i] = valid ? t - qlo + i * QT : 0;
+                        stq[i] = valid && u != r && u != s;        // rows r, s: touching lanes
+                        d4[i] = *reinterpret_cast<const int4*>(cs.D + 4 * gq[i]);
+                        pu[i] = stg[u];
+                        DB::load4(stg, v0q[i], pv[i]);
+                    }
+#pragma unroll
+                    for (int i = 0; i < QP; ++i) {
+                        const int4 nv = make_int4(d4[i].x + DB::rank(pu[i], pv[i][0]),
+                                                  d4[i].y + DB::rank(pu[i], pv[i][1]),
+                                                  d4[i].z + DB::rank(pu[i], pv[i][2]),
+                                                  d4[i].w + DB::rank(pu[i], pv[i][3]));
+                        const unsigned er = (unsigned)(r - v0q[i]), es = (unsigned)(s - v0q[i]);
+                        const int g = gq[i];
+                        if (stq[i] && er >= 4u && es >= 4u) {
+                            *reinterpret_cast<int4*>(cs.D + 4 * g) = nv;
+                        } else if (stq[i]) {          // columns r/s belong to the touching lanes
+                            if (er != 0u && es != 0u) cs.D[4 * g + 0] = nv.x;
+                            if (er != 1u && es != 1u) cs.D[4 * g + 1] = nv.y;
+                            if (er != 2u && es != 2u) cs.D[4 * g + 2] = nv.z;
+                            if (er != 3u && es != 3u) cs.D[4 * g + 3] = nv.w;
+                        }
+                    }
                 } else {
                     for (int g = t - qlo; g < nqt; g += QT) quad(tb.qdesc[g], g);
                 }
             }
+            // address and threshold of this thread's candidate in the next window
+            // (the window lanes are the last warps: quad warps, after their quads)
+            if (off < Wnext && kacc + 1 + (uint64_t)off < k_end) {
+                prepare_addr(pre, n, tb.rowaddr, advance_cursor(cur, j + 1 + off, M),
+                             kacc + 1 + (uint64_t)off);
+                prepare_theta(pre, sch, seed, chain);
+            }
+#ifdef QAPSA_PHASE_TIMERS
+            if (t == 0) atomicAdd(&g_phase_cycles[13], (unsigned long long)(clock_after((int)pre.th) - pt1));
+            if (t == qlo) atomicAdd(&g_phase_cycles[14], (unsigned long long)(clock_after(cs.D[4 * (t - qlo)]) - pt1));
+            if (t == NT - 1) atomicAdd(&g_phase_cycles[15], (unsigned long long)(clock_after(cs.D[4 * (t - qlo)]) - pt1));
+#endif
             if (scalar_thread) {                  // scalar state: p, C, best, digest, Δ_rs
                 const uint16_t pr = cs.p[r];
                 cs.p[r] = cs.p[s];
@@ -522,15 +603,17 @@ __device__ __forceinline__ uint64_t chain_run(const TA* __restrict__ A, const Ch
         pend_r = r;
         pend_s = s;
         group_sync(bar_id, NT);
-        PT_MARK(pt3);
         PT_ADD(0, pt0, pt1);
-        PT_ADD(2, pt1, pt3);
         PT_ADD(4, 0, 1);
+#ifdef QAPSA_PHASE_TIMERS
+        su_start = pt1;
+#endif
 
         ++accepted;
         k = kacc + 1;
         cur = advance_cursor(cur, j + 1, M);
         W = Wnext;
+        rejT = 38.5f * temp32(sch, k);
     }
     // the B' exchange of the last accept is not needed (B' is rebuilt from p at the next
     // launch); its best_p copy is

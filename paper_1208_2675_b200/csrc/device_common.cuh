@@ -43,6 +43,7 @@ struct Sched {
     double t0;
     double coef;
     float t0f;     // (float)t0
+    float coeff;   // (float)coef
 };
 
 __device__ __forceinline__ double temperature(const Sched& s, uint64_t k) {
@@ -52,10 +53,12 @@ __device__ __forceinline__ double temperature(const Sched& s, uint64_t k) {
 }
 
 // T_k in float, relative error < 2e-6: only brackets decisions (never decides alone).
+// Float only (no FP64 on the fast path): coef and k each rounded to float, so the
+// exponent carries a relative error ~2e-7; with __expf T32 is within ~2e-6 of T_k.
 __device__ __forceinline__ float temp32(const Sched& s, uint64_t k) {
-    const double x = __dmul_rn(s.coef, (double)k);
-    if (s.kind == 1) return __fdividef(s.t0f, 1.0f + (float)x * s.t0f);
-    return s.t0f * __expf((float)x);
+    const float x = s.coeff * __ull2float_rn(k);
+    if (s.kind == 1) return __fdividef(s.t0f, 1.0f + x * s.t0f);
+    return s.t0f * __expf(x);
 }
 
 // ---- Eq.(2) acceptance for one candidate in the "live band" (0 < delta <= 38 T):
@@ -88,12 +91,17 @@ __host__ __device__ __forceinline__ int tri_index(int n, int r, int s) {
     return tri_base(n, r) + (s - r - 1);
 }
 // q -> (r, s); closed form guess corrected by integer checks.
+// The closed form r = floor((b - sqrt(b^2 - 8q)) / 2), b = 2n-1, with the approximate
+// MUFU square root (error << 1e-3 for b^2 - 8q < 2^24), is off by at most one;
+// one branch-free correction each way makes it exact.
 __device__ __forceinline__ void tri_pair(int n, int q, int* r, int* s) {
-    const int b = 2 * n - 1;                       // b*b - 8q < 2^24: exact in float
-    int rr = (int)((float)b - sqrtf((float)(b * b - 8 * q))) >> 1;
+    const int b = 2 * n - 1;
+    float sq;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(sq) : "f"((float)(b * b - 8 * q)));
+    int rr = (int)(((float)b - sq) * 0.5f);
     rr = max(0, min(rr, n - 2));
-    while (rr > 0 && tri_base(n, rr) > q) --rr;
-    while (rr < n - 2 && tri_base(n, rr + 1) <= q) ++rr;
+    rr = (rr > 0 && tri_base(n, rr) > q) ? rr - 1 : rr;
+    rr = (rr < n - 2 && tri_base(n, rr + 1) <= q) ? rr + 1 : rr;
     *r = rr;
     *s = q - tri_base(n, rr) + rr + 1;
 }

@@ -147,6 +147,7 @@ static qap_status validate_schedule(qap_ctx* c, const qap_schedule* s, uint64_t 
         out->coef = s->total_iters > 1 ? std::log(s->tf / s->t0) / I1 : 0.0;
     else
         out->coef = s->total_iters > 1 ? (s->t0 - s->tf) / ((I1 * s->t0) * s->tf) : 0.0;
+    out->coeff = (float)out->coef;
     return QAP_OK;
 }
 
@@ -357,9 +358,9 @@ static cudaError_t launch_generic(qap_ctx* c, const ChainArgs& a, bool ds, int s
 
 // Threads of the single-chain CTA: enough for 4 lanes per touching v and <= 3 quads per thread.
 // Threads of the single-chain CTA: touching warps (8 v each) plus quad warps with
-// <= 3 quads per thread, rounded to a power of two.
+// <= 4 quads per thread, rounded to a power of two.
 static int auto_threads(const qap_ctx* c) {
-    const int need = 32 * touch_warps(c->n) + (c->nqt + 2) / 3;
+    const int need = 32 * touch_warps(c->n) + (c->nqt + 3) / 4;
     int nt = 64;
     while (nt < 1024 && nt < need) nt *= 2;
     return nt;
@@ -369,10 +370,12 @@ static int auto_threads(const qap_ctx* c) {
 // configurations; everything else runs the generic instance of the same code.
 static cudaError_t launch_chain(qap_ctx* c, const ChainArgs& a, int threads, bool explicit_threads,
                                 bool ds, int smem) {
-    if (!explicit_threads) {
+    (void)explicit_threads;
+    {
         if (c->ta == 1 && c->tb == 1 && ds) {
-            if (c->n == 12 && threads == 128) return launch_chain_t<uint8_t, uint8_t, 128, true, 12>(c, a, smem);
-            if (c->n == 50 && threads == 512) return launch_chain_t<uint8_t, uint8_t, 512, true, 50>(c, a, smem);
+            if (c->n == 12 && threads == 64) return launch_chain_t<uint8_t, uint8_t, 64, true, 12>(c, a, smem);
+            if (c->n == 50 && threads == 256) return launch_chain_t<uint8_t, uint8_t, 256, true, 50>(c, a, smem);
+            if (c->n == 100 && threads == 512) return launch_chain_t<uint8_t, uint8_t, 512, true, 100>(c, a, smem);
             if (c->n == 100 && threads == 1024) return launch_chain_t<uint8_t, uint8_t, 1024, true, 100>(c, a, smem);
         }
         if (c->ta == 1 && c->tb == 2 && !ds && c->n == 256 && threads == 1024)
@@ -634,8 +637,8 @@ qap_status qap_ensemble_run(qap_ctx* c, uint32_t chain_begin, uint32_t chain_cou
 #ifdef QAPSA_PHASE_TIMERS
 // debug build only (not part of include/qapsa.h): read-and-clear the phase cycle counters
 int qapsa_debug_phase_cycles(unsigned long long* out8) {
-    if (cudaMemcpyFromSymbol(out8, g_phase_cycles, 8 * sizeof(unsigned long long)) != cudaSuccess) return 1;
-    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (cudaMemcpyFromSymbol(out8, g_phase_cycles, 16 * sizeof(unsigned long long)) != cudaSuccess) return 1;
+    unsigned long long z[16] = {0};
     return cudaMemcpyToSymbol(g_phase_cycles, z, sizeof z) != cudaSuccess;
 }
 #endif

@@ -19,13 +19,18 @@ s.delta_init()
 t0, tf = s.schedule_bounds()
 sch = Q.make_schedule(0, t0, tf, cfg["iters"])
 L = Q.lib()
-buf = (C.c_ulonglong * 8)()
+buf = (C.c_ulonglong * 16)()
 L.qapsa_debug_phase_cycles(buf)
 g = s.run(0, iters, sch, SA_SEED)
 ms, _ = s.last_kernel_time()
 L.qapsa_debug_phase_cycles(buf)
 w_acc, w_no, S, U, nacc, nno = buf[0], buf[1], buf[2], buf[3], buf[4], buf[5]
+tdone, qdone = buf[6], buf[7]
 print(f"iters {iters:.0e} threads {threads or 'auto'}: {ms:.1f} ms, accepts {g['accepted']}, "
       f"{ms*1e6/max(1,g['accepted']):.0f} ns/accept")
-print(f"  per accept: W {w_acc/max(1,nacc):.0f} clk, S {S/max(1,nacc):.0f} clk, U {U/max(1,nacc):.0f} clk;"
+print(f"  per accept: W {w_acc/max(1,nacc):.0f} clk, SU {S/max(1,nacc):.0f} clk (stage released {U/max(1,nacc):.0f}, "
+      f"W: offset-0 candidate done {tdone/max(1,nacc):.0f}, exchange done {qdone/max(1,nacc):.0f});"
       f"  non-accepting windows: {nno} x {w_no/max(1,nno):.0f} clk")
+print(f"  W-phase prepare_addr {buf[8]}, prepare_theta {buf[9]}, exact double path {buf[10]} (of {iters} iterations)")
+print(f"  W: thread 0 reaches its candidate at {buf[11]/max(1,nacc):.0f} clk after the loop top")
+print(f"  SU: t0 dots done {buf[12]/max(1,nacc):.0f}, t0 incl. prep {buf[13]/max(1,nacc):.0f}, quads done: first thread {buf[14]/max(1,nacc):.0f}, last thread {buf[15]/max(1,nacc):.0f}")
