@@ -181,9 +181,15 @@ typedef enum {
     QAP_OPT_WINDOW_MAX = 1,      /* max candidates per window, 32..1024 (default 1024) */
     QAP_OPT_THREADS = 2,         /* single-chain CTA threads: 0 = auto (default), 64..1024 */
     QAP_OPT_FORCE_GLOBAL_DELTA = 3, /* 1: keep Δ in global memory/L2 even if it fits on chip */
-    QAP_OPT_ENSEMBLE_GROUP = 4   /* threads per chain in qap_ensemble_run: 64, 128 or 256 */
+    QAP_OPT_ENSEMBLE_GROUP = 4,  /* threads per chain in qap_ensemble_run: 64, 128 or 256 */
+    QAP_OPT_TENSOR_CORE = 5      /* qap_sa_run engine: 1 (default) = Δ in tensor memory with the
+                                    rank update on the tensor cores when the instance allows it
+                                    (4 <= n <= 128, all entries <= 127), else the shared-memory
+                                    kernel; 0 = always the shared-memory kernel */
 } qap_option;
 qap_status qap_set_option(qap_ctx* ctx, int32_t key, int64_t value);
+/* 1 if the next qap_sa_run uses the tensor-memory engine (QAP_OPT_TENSOR_CORE), else 0. */
+int32_t qap_uses_tensor_core(const qap_ctx* ctx);
 
 /* Device time in milliseconds of the last qap_sa_run kernel (CUDA events
  * on the context stream), and the number of kernels the last call launched. */

@@ -250,7 +250,7 @@ __device__ __forceinline__ void stage_wait(int id, int nthreads) {
 // Optional phase timers (debug build with -DQAPSA_PHASE_TIMERS, tools/phase_times.py):
 // cycles spent by thread 0 of the group in W (accepting / non-accepting windows) and SU.
 #ifdef QAPSA_PHASE_TIMERS
-__device__ unsigned long long g_phase_cycles[16];
+__device__ unsigned long long g_phase_cycles[128];
 #define PT_COUNT(slot) atomicAdd(&g_phase_cycles[slot], 1ull)
 // clock read that waits for `dep` (a shared-memory value read after a barrier): with
 // BAR.SYNC.DEFER_BLOCKING a plain clock read would be issued before the barrier releases

@@ -16,6 +16,7 @@
 
 #include "../../include/qapsa.h"
 #include "kernels.cuh"
+#include "tc_chain.cuh"
 
 using namespace qapsa;
 
@@ -46,6 +47,8 @@ struct qap_ctx {
     std::string err;
     int wmax = 1024, threads = 0 /* auto */, force_global = 0, ens_group = 128;
     int smem_optin = 0, num_sms = 0;
+    bool tc_ok = false;                 // instance fits the tensor-memory engine (tc_chain.cuh)
+    int use_tc = 1;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     float last_ms = 0.f;
     int last_launches = 0;
@@ -107,6 +110,8 @@ static std::vector<unsigned char> compact(int n, int ld, const int32_t* X) {
         for (int j = 0; j < n; ++j) o[(size_t)i * ld + j] = (T)X[(size_t)i * n + j];
     return out;
 }
+
+static bool use_tc_engine(const qap_ctx* c) { return c->tc_ok && c->use_tc && !c->force_global; }
 
 static int dab_bytes(const qap_ctx* c) { return (c->ta == 1 && c->tb == 1) ? 4 : 8; }
 
@@ -233,6 +238,7 @@ qap_status qap_create(int32_t n, const int32_t* A, const int32_t* B, const int32
     c->stream = (cudaStream_t)stream;
     c->ta = maxA <= 255 ? 1 : 2;
     c->tb = maxB <= 255 ? 1 : 2;
+    c->tc_ok = tc_eligible(n, maxA, maxB);
     c->smem_optin = (int)prop.sharedMemPerBlockOptin;
     std::vector<int32_t> hrow;
     std::vector<uint16_t> hq;
@@ -419,10 +425,11 @@ qap_status qap_sa_run(qap_ctx* c, uint64_t k0, uint64_t iters, const qap_schedul
     CU(cudaMemcpyAsync(&before, c->dst, sizeof before, cudaMemcpyDeviceToHost, c->stream));
     CU(cudaMemcpyAsync(&near_before, c->dnear_count, sizeof near_before, cudaMemcpyDeviceToHost, c->stream));
 
+    const bool tc = use_tc_engine(c);
     const bool explicit_threads = c->threads != 0;
-    const int threads = effective_threads(c, explicit_threads ? c->threads : auto_threads(c));
+    const int threads = tc ? TCK_NT : effective_threads(c, explicit_threads ? c->threads : auto_threads(c));
     bool ds = !c->force_global && chain_smem_bytes(c, threads, true) <= c->smem_optin;
-    const int smem = chain_smem_bytes(c, threads, ds);
+    const int smem = tc ? tc_layout(c->ld).bytes : chain_smem_bytes(c, threads, ds);
     if (smem > c->smem_optin) return fail(c, QAP_E_UNSUPPORTED, "chain state does not fit on chip");
 
     ChainArgs a;
@@ -434,7 +441,16 @@ qap_status qap_sa_run(qap_ctx* c, uint64_t k0, uint64_t iters, const qap_schedul
     a.k0 = k0; a.k_end = k0 + iters; a.seed = seed; a.sch = sch;
 
     CU(cudaEventRecord(c->ev0, c->stream));
-    CU(launch_chain(c, a, threads, explicit_threads, ds, smem));
+    if (tc) {
+        a.wmax = c->wmax;
+        // compile-time problem size for the BASELINE configurations, generic otherwise
+        auto kern = c->n == 100 ? k_sa_tc<100> : c->n == 50 ? k_sa_tc<50> : c->n == 12 ? k_sa_tc<12> : k_sa_tc<0>;
+        CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        kern<<<1, TCK_NT, smem, c->stream>>>(a);
+        CU(cudaGetLastError());
+    } else {
+        CU(launch_chain(c, a, threads, explicit_threads, ds, smem));
+    }
     CU(cudaEventRecord(c->ev1, c->stream));
     DevState after;
     unsigned int near_after = 0;
@@ -637,8 +653,8 @@ qap_status qap_ensemble_run(qap_ctx* c, uint32_t chain_begin, uint32_t chain_cou
 #ifdef QAPSA_PHASE_TIMERS
 // debug build only (not part of include/qapsa.h): read-and-clear the phase cycle counters
 int qapsa_debug_phase_cycles(unsigned long long* out8) {
-    if (cudaMemcpyFromSymbol(out8, g_phase_cycles, 16 * sizeof(unsigned long long)) != cudaSuccess) return 1;
-    unsigned long long z[16] = {0};
+    if (cudaMemcpyFromSymbol(out8, g_phase_cycles, 128 * sizeof(unsigned long long)) != cudaSuccess) return 1;
+    unsigned long long z[128] = {0};
     return cudaMemcpyToSymbol(g_phase_cycles, z, sizeof z) != cudaSuccess;
 }
 #endif
@@ -658,6 +674,9 @@ qap_status qap_set_option(qap_ctx* c, int32_t key, int64_t value) {
         case QAP_OPT_FORCE_GLOBAL_DELTA:
             c->force_global = value ? 1 : 0;
             return QAP_OK;
+        case QAP_OPT_TENSOR_CORE:
+            c->use_tc = value ? 1 : 0;
+            return QAP_OK;
         case QAP_OPT_ENSEMBLE_GROUP:
             if (value != 64 && value != 128 && value != 256) return fail(c, QAP_E_INVALID_ARG, "group must be 64, 128 or 256");
             c->ens_group = (int)value;
@@ -665,6 +684,8 @@ qap_status qap_set_option(qap_ctx* c, int32_t key, int64_t value) {
     }
     return fail(c, QAP_E_INVALID_ARG, "unknown option");
 }
+
+int32_t qap_uses_tensor_core(const qap_ctx* c) { return (c && use_tc_engine(c)) ? 1 : 0; }
 
 qap_status qap_last_kernel_time(qap_ctx* c, float* ms, int32_t* launches) {
     CHECK_CTX(c);

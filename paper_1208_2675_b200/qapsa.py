@@ -22,13 +22,14 @@ STATUS = {0: "QAP_OK", 1: "QAP_E_INVALID_ARG", 2: "QAP_E_DIMENSION", 3: "QAP_E_U
           9: "QAP_E_NOMEM"}
 QAP_COOL_GEOMETRIC, QAP_COOL_LUNDY_MEES = 0, 1
 QAP_OPT_WINDOW_MAX, QAP_OPT_THREADS, QAP_OPT_FORCE_GLOBAL_DELTA, QAP_OPT_ENSEMBLE_GROUP = 1, 2, 3, 4
+QAP_OPT_TENSOR_CORE = 5
 QAP_NEAR_LOG_CAP = 1024
 
 # Every symbol include/qapsa.h declares (checked by tests/test_abi.py).
 EXPORTS = ("qap_create", "qap_destroy", "qap_reset", "qap_delta_init", "qap_sa_run", "qap_cost",
            "qap_get_state", "qap_get_near_ties", "qap_schedule_bounds", "qap_ensemble_run",
-           "qap_set_option", "qap_last_kernel_time", "qap_status_str", "qap_last_error",
-           "qap_version")
+           "qap_set_option", "qap_uses_tensor_core", "qap_last_kernel_time", "qap_status_str",
+           "qap_last_error", "qap_version")
 
 
 class QapError(RuntimeError):
@@ -93,8 +94,11 @@ def lib(build_if_missing: bool = True):
     L.qap_last_error.argtypes = [vp]
     L.qap_last_error.restype = C.c_char_p
     L.qap_version.restype = C.c_int32
+    L.qap_uses_tensor_core.argtypes = [vp]
+    L.qap_uses_tensor_core.restype = C.c_int32
     for name in EXPORTS:
-        if name not in ("qap_destroy", "qap_status_str", "qap_last_error", "qap_version"):
+        if name not in ("qap_destroy", "qap_status_str", "qap_last_error", "qap_version",
+                        "qap_uses_tensor_core"):
             getattr(L, name).restype = C.c_int
     _lib = L
     return L
@@ -219,6 +223,10 @@ def qap_set_option(ctx, key, value):
     _check(lib().qap_set_option(ctx, key, value), ctx)
 
 
+def qap_uses_tensor_core(ctx) -> bool:
+    return bool(lib().qap_uses_tensor_core(ctx))
+
+
 def qap_last_kernel_time(ctx):
     ms, nl = C.c_float(), C.c_int32()
     _check(lib().qap_last_kernel_time(ctx, C.byref(ms), C.byref(nl)), ctx)
@@ -288,6 +296,9 @@ class Solver:
 
     def set_option(self, key, value):
         qap_set_option(self.ctx, key, value)
+
+    def uses_tensor_core(self) -> bool:
+        return qap_uses_tensor_core(self.ctx)
 
     def ensemble(self, chain_begin, p0s, iters, schedule, seed, per_chain=False):
         return qap_ensemble_run(self.ctx, chain_begin, p0s, iters, schedule, seed, per_chain)

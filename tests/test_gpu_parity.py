@@ -16,6 +16,11 @@ if not torch.cuda.is_available():
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
 
+TC = Q.QAP_OPT_TENSOR_CORE
+# both single-chain engines: Δ in tensor memory (default where eligible) and Δ in shared memory
+ENGINES = [pytest.param(1, id="tmem"), pytest.param(0, id="smem")]
+
+
 def _sched(s: O.Schedule):
     return Q.make_schedule(s.kind, s.t0, s.tf, s.total_iters)
 
@@ -100,17 +105,63 @@ def test_reset_restores_p0_and_perm():
 
 # ---------------- a2-a7: full trajectories ----------------
 
-def test_config1_full_bit_exact():
+@pytest.mark.parametrize("engine", ENGINES)
+def test_config1_full_bit_exact(engine):
     A, B, p0, cfg = config(1)
     sch = O.geometric_schedule_for(A, B, p0, cfg["iters"])
-    g, acc = _compare_run(A, B, p0, cfg["iters"], sch)
+    g, acc = _compare_run(A, B, p0, cfg["iters"], sch, opts=[(TC, engine)])
     assert acc > 100
 
 
-def test_config2_full_bit_exact():
+@pytest.mark.parametrize("engine", ENGINES)
+def test_config2_full_bit_exact(engine):
     A, B, p0, cfg = config(2)
     sch = O.geometric_schedule_for(A, B, p0, cfg["iters"])
-    _compare_run(A, B, p0, cfg["iters"], sch, mode=O.MODE_SCRATCH)
+    _compare_run(A, B, p0, cfg["iters"], sch, mode=O.MODE_SCRATCH, opts=[(TC, engine)])
+
+
+def test_engine_selection():
+    """The tensor-memory engine runs exactly on the eligible instances (n <= 128, entries <= 127)."""
+    cases = [(taixxa(100, 1), True), (taixxa(128, 2), True), (taixxa(129, 3), False),
+             (taixxa(3, 4), False), (grey_density(256), False)]
+    for (A, B), want in cases:
+        with Q.Solver(A, B, start_perm(A.shape[0], 1, 0)) as s:
+            assert s.uses_tensor_core() == want
+            s.set_option(TC, 0)
+            assert not s.uses_tensor_core()
+    A, B = taixxa(20, 5)
+    B2 = B.copy()
+    B2[0, 1] = B2[1, 0] = 128
+    with Q.Solver(A, B2, start_perm(20, 1, 0)) as s:
+        assert not s.uses_tensor_core()
+
+
+@pytest.mark.parametrize("n,seed", [(4, 1), (31, 2), (32, 3), (33, 4), (64, 5), (97, 6), (127, 7),
+                                    (128, 8)])
+def test_tmem_engine_full_range_values(n, seed):
+    """Entries spanning the whole eligible range [0, 127] (the 8-bit digit encoding of the
+    rank update at its limits) and sizes around the 32-lane TMEM quadrants."""
+    rng = np.random.default_rng(seed)
+    A = rng.integers(0, 128, size=(n, n)).astype(np.int32)
+    B = rng.integers(0, 128, size=(n, n)).astype(np.int32)
+    A = np.triu(A, 1); A = A + A.T
+    B = np.triu(B, 1); B = B + B.T
+    A[0, n - 1] = A[n - 1, 0] = 127
+    B[0, n - 1] = B[n - 1, 0] = 127
+    p0 = start_perm(n, seed, 0)
+    sch = O.geometric_schedule_for(A, B, p0, 60000)
+    with Q.Solver(A, B, p0) as s:
+        assert s.uses_tensor_core()
+    g, acc = _compare_run(A, B, p0, 60000, sch)
+    assert acc > 100
+
+
+@pytest.mark.parametrize("wmax", [32, 64, 256, 1024])
+def test_tmem_window_invariance(wmax):
+    A, B = taixxa(100, 77)
+    p0 = start_perm(100, 5, 0)
+    sch = O.geometric_schedule_for(A, B, p0, 200000)
+    _compare_run(A, B, p0, 200000, sch, opts=[(Q.QAP_OPT_WINDOW_MAX, wmax)])
 
 
 @pytest.mark.parametrize("threads,wmax", [(256, 32), (512, 128), (1024, 1024), (1024, 64),
@@ -120,16 +171,17 @@ def test_window_and_cta_shape_invariance(threads, wmax):
     A, B = taixxa(50, 77)
     p0 = start_perm(50, 5, 0)
     sch = O.geometric_schedule_for(A, B, p0, 200000)
-    _compare_run(A, B, p0, 200000, sch, opts=[(Q.QAP_OPT_THREADS, threads),
+    _compare_run(A, B, p0, 200000, sch, opts=[(TC, 0), (Q.QAP_OPT_THREADS, threads),
                                                 (Q.QAP_OPT_WINDOW_MAX, wmax)])
 
 
-def test_resume_split_calls():
+@pytest.mark.parametrize("engine", ENGINES)
+def test_resume_split_calls(engine):
     A, B = taixxa(37, 9)
     p0 = start_perm(37, 9, 0)
     I = 300000
     sch = O.geometric_schedule_for(A, B, p0, I)
-    _compare_run(A, B, p0, I, sch, k_splits=[0, 1, 999, 1000, 123457, I])
+    _compare_run(A, B, p0, I, sch, k_splits=[0, 1, 999, 1000, 123457, I], opts=[(TC, engine)])
 
 
 def test_global_delta_variant():
@@ -140,38 +192,43 @@ def test_global_delta_variant():
     _compare_run(A, B, p0, 200000, sch, opts=[(Q.QAP_OPT_FORCE_GLOBAL_DELTA, 1)])
 
 
-def test_lundy_mees_schedule():
+@pytest.mark.parametrize("engine", ENGINES)
+def test_lundy_mees_schedule(engine):
     A, B = taixxa(30, 30)
     p0 = start_perm(30, 1, 0)
     g = O.geometric_schedule_for(A, B, p0, 100000)
     sch = O.Schedule(O.COOL_LUNDY_MEES, g.t0, g.tf, 100000)
-    _compare_run(A, B, p0, 100000, sch)
+    _compare_run(A, B, p0, 100000, sch, opts=[(TC, engine)])
 
 
+@pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("n", [2, 3, 4, 5, 7])
-def test_tiny_instances_window_wraps(n):
+def test_tiny_instances_window_wraps(n, engine):
     """M < window: candidates wrap around the triangle many times per window."""
     A, B = taixxa(n, 40 + n)
     p0 = start_perm(n, n, 0)
     sch = O.geometric_schedule_for(A, B, p0, 20000)
-    _compare_run(A, B, p0, 20000, sch)
+    _compare_run(A, B, p0, 20000, sch, opts=[(TC, engine)])
 
 
-def test_all_zero_flow_every_iteration_accepts():
+@pytest.mark.parametrize("engine", ENGINES)
+def test_all_zero_flow_every_iteration_accepts(engine):
     n = 16
     _, B = taixxa(n, 2)
     A = np.zeros((n, n), np.int32)
     p0 = start_perm(n, 1, 0)
     sch = O.Schedule(O.COOL_GEOMETRIC, 1.0, 0.1, 5000)
-    g, acc = _compare_run(A, B, p0, 5000, sch)
+    g, acc = _compare_run(A, B, p0, 5000, sch, opts=[(TC, engine)])
     assert acc == 5000 and g["cost"] == 0
 
 
-def test_single_iteration_and_tail_of_schedule():
+@pytest.mark.parametrize("engine", ENGINES)
+def test_single_iteration_and_tail_of_schedule(engine):
     A, B = taixxa(25, 2)
     p0 = start_perm(25, 2, 0)
     sch = O.geometric_schedule_for(A, B, p0, 10**6)
     with Q.Solver(A, B, p0) as s:
+        s.set_option(TC, engine)
         s.delta_init()
         g = s.run(10**6 - 1, 1, _sched(sch), 7)
         _, _, D = s.state()

@@ -19,7 +19,7 @@ s.delta_init()
 t0, tf = s.schedule_bounds()
 sch = Q.make_schedule(0, t0, tf, cfg["iters"])
 L = Q.lib()
-buf = (C.c_ulonglong * 16)()
+buf = (C.c_ulonglong * 128)()
 L.qapsa_debug_phase_cycles(buf)
 g = s.run(0, iters, sch, SA_SEED)
 ms, _ = s.last_kernel_time()

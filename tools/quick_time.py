@@ -15,7 +15,8 @@ s = Q.Solver(A, B, p0)
 s.delta_init()
 t0, tf = s.schedule_bounds()
 sch = Q.make_schedule(0, t0, tf, I)
-for thr in (1024, 512):
+for eng, thr in ((1, 0), (0, 512)):
+    s.set_option(Q.QAP_OPT_TENSOR_CORE, eng)
     s.set_option(Q.QAP_OPT_THREADS, thr)
     for frac in (10, 1):
         s.reset(); s.delta_init()
@@ -24,8 +25,10 @@ for thr in (1024, 512):
         g = s.run(0, n, sch, SA_SEED)
         dt = time.time() - t
         ms, _ = s.last_kernel_time()
-        print(f"threads={thr} iters={n:.0e} kernel {ms:.1f} ms wall {dt*1e3:.1f} ms "
+        print(f"engine={'tmem' if s.uses_tensor_core() else 'smem'} threads={thr} iters={n:.0e} kernel {ms:.1f} ms wall {dt*1e3:.1f} ms "
               f"{n/(ms/1e3):.3e} it/s acc={g['accepted']} best={g['best_cost']}", flush=True)
+if "--no-ens" in sys.argv:
+    sys.exit(0)
 A5, B5, _, c5 = config(5)
 for chains, iters in ((1036, 10**6), (8192, 10**6)):
     p0s = start_perms(100, SA_SEED, 0, chains)
