@@ -115,11 +115,12 @@ def measured_peaks():
         return {}
 
 
-def profile_traffic():
+def profile_traffic(which):
     """Per-launch dram bytes of the dominant kernel from the committed ncu summary, if any."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
-            return json.load(f).get("sa_chain_dram_bytes_per_launch")
+            d = json.load(f)
+        return d.get("sa_tc_dram_bytes_per_launch" if which == "tc" else "sa_chain_dram_bytes_per_launch")
     except Exception:
         return None
 
@@ -240,21 +241,47 @@ def run_ours(args):
     acc = stats[-1]["accepted"]
     clocks = clk.summary()
 
-    # roofline of the dominant kernel (k_sa_chain): algorithmic on-chip bytes / its duration
-    sa = s_ta = 1
+    # roofline of the dominant kernel.  Tensor-memory engine (k_sa_tc): every
+    # accepted swap is two int8 tensor-core MMAs (Δ += L R^T: 128x128x32; [G|H] += 128x256x32), the
+    # algorithmic O(N^2) work of the update; peak = one SM's share of the dense int8 tensor peak
+    # (the chain runs on one SM).  Shared-memory engine (k_sa_chain): algorithmic on-chip bytes
+    # against one SM's shared-memory bandwidth.
     kms = statistics.mean(kern_ms)
-    algo_bytes = BYTES_PER_PROPOSAL * I + acc * bytes_per_accept(n, sa, s_ta)
-    achieved = algo_bytes / (kms / 1e3) / 1e9
     peaks = measured_peaks()
     mhz = peaks.get("sm_max_mhz", 1965.0)
-    peak = SMEM_BYTES_PER_CLK * mhz * 1e6 / 1e9   # one SM: the chain runs on one SM
-    roofline = {"bound": "smem", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": profile_traffic(),
-                "kernel": "k_sa_chain", "kernel_ms": kms,
-                "peak_source": f"128 B/clk/SM (B300_MICROARCH.md) x sm_max_mhz {mhz} "
-                               f"(MEASURED_PEAKS.json), one SM",
-                "algorithmic_bytes_per_launch": algo_bytes,
-                "share_of_step": kms / ms_per_step}
+    sms = peaks.get("sm_count", 148)
+    if s.uses_tensor_core():
+        ops_per_accept = 2 * 128 * (128 + 256) * 32
+        algo = acc * ops_per_accept
+        achieved = algo / (kms / 1e3) / 1e12
+        bf16 = peaks.get("bf16_tflops")          # burst: the chain kernel is timed on its own
+        if bf16:
+            chip_i8, src = 2.0 * float(bf16), ("of measured: MEASURED_PEAKS.json bf16_tflops x 2 "
+                                               "(int8:bf16 nominal ratio 4.5:2.25)")
+        else:
+            chip_i8, src = 2.0 * 1590.0, "of fallback: 1.59 PFLOP/s bf16 (B200_PROFILING.md) x 2"
+        peak = chip_i8 / sms
+        roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS (int8)",
+                    "frac": achieved / peak, "traffic": profile_traffic("tc"),
+                    "kernel": "k_sa_tc", "kernel_ms": kms,
+                    "peak_source": f"{src}, one SM of {sms}",
+                    "algorithmic_ops_per_launch": algo,
+                    "ops_per_accept": ops_per_accept,
+                    "share_of_step": kms / ms_per_step,
+                    "note": "latency-bound sequential chain: per accept the tensor cores run ~0.25 us of "
+                            "MMA; the rest of the accept is the window/stage/patch dependency chain"}
+    else:
+        sa = s_ta = 1
+        algo_bytes = BYTES_PER_PROPOSAL * I + acc * bytes_per_accept(n, sa, s_ta)
+        achieved = algo_bytes / (kms / 1e3) / 1e9
+        peak = SMEM_BYTES_PER_CLK * mhz * 1e6 / 1e9   # one SM: the chain runs on one SM
+        roofline = {"bound": "smem", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": profile_traffic("chain"),
+                    "kernel": "k_sa_chain", "kernel_ms": kms,
+                    "peak_source": f"128 B/clk/SM (B300_MICROARCH.md) x sm_max_mhz {mhz} "
+                                   f"(MEASURED_PEAKS.json), one SM",
+                    "algorithmic_bytes_per_launch": algo_bytes,
+                    "share_of_step": kms / ms_per_step}
 
     # e2e through the public API with host buffers (create copies A, B, p0; state read back)
     e2e_ms = []
@@ -289,6 +316,7 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "int32+f64",
             "data": "synthetic (seeded tai100a-shaped instance, BASELINE config 3)",
+            "engine": "tensor-memory (k_sa_tc)" if s.uses_tensor_core() else "shared-memory (k_sa_chain)",
             "config": {"workload": "config3 tai100a-shaped N=100, 1 chain, 1e8 iterations"
                                    + (" (one replica per rank)" if ws > 1 else ""),
                        "n": n, "iters_per_step": I, "chains_per_rank": 1,

@@ -1,5 +1,5 @@
 #!/bin/bash
-# One GPU-box session: tests, bench, ncu launch list + full capture (see B200_PROFILING.md).
+# One GPU-box session: tests, bench, ncu launch list + full captures (see B200_PROFILING.md).
 # Usage (via gpurun): bash tools/gpu_round.sh [tag]
 set -u
 TAG=${1:-r01}
@@ -11,12 +11,12 @@ timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=
 timeout 600 python bench.py --impl reference --steps 1 --warmup 0 > $OUT/bench_ref.json 2> $OUT/bench_ref.err
 # launch list of the timed single-chain workload (same command plain, then under ncu)
 CMD="python bench.py --steps 2 --warmup 3 --no-ensemble --no-cpu-baseline --e2e-steps 1"
-$CMD > $OUT/plain.log 2>&1 && \
+timeout 300 $CMD > $OUT/plain.log 2>&1 && \
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file $OUT/launches_$TAG.csv $CMD > $OUT/ncu_launch.log 2>&1
 echo "launches rc=$?" >> $OUT/ncu_launch.log
-# full capture of the dominant kernel on a short run of the same kernel
-python tools/prof_chain.py 1e5 > $OUT/prof_plain.log 2>&1 && \
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_sa_chain -c 1 \
-    -o $OUT/prof_sa_chain_$TAG python tools/prof_chain.py 1e5 > $OUT/ncu_full.log 2>&1
+# full capture of the dominant kernel (tensor-memory engine) on a short run of config 3
+timeout 120 python tools/run_cfg3.py 2e5 > $OUT/prof_plain.log 2>&1 && \
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_sa_tc -c 1 \
+    -o $OUT/prof_sa_tc_$TAG python tools/run_cfg3.py 2e5 > $OUT/ncu_full.log 2>&1
 echo "full rc=$?" >> $OUT/ncu_full.log
