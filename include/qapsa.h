@@ -182,10 +182,14 @@ typedef enum {
     QAP_OPT_THREADS = 2,         /* single-chain CTA threads: 0 = auto (default), 64..1024 */
     QAP_OPT_FORCE_GLOBAL_DELTA = 3, /* 1: keep Δ in global memory/L2 even if it fits on chip */
     QAP_OPT_ENSEMBLE_GROUP = 4,  /* threads per chain in qap_ensemble_run: 64, 128 or 256 */
-    QAP_OPT_TENSOR_CORE = 5      /* qap_sa_run engine: 1 (default) = Δ in tensor memory with the
+    QAP_OPT_TENSOR_CORE = 5,     /* qap_sa_run engine: 1 (default) = Δ in tensor memory with the
                                     rank update on the tensor cores when the instance allows it
                                     (4 <= n <= 128, all entries <= 127), else the shared-memory
                                     kernel; 0 = always the shared-memory kernel */
+    QAP_OPT_SCRATCH_PHASE = 6    /* tensor-memory engine only: 1 (default) = run the high-acceptance
+                                    start of each qap_sa_run without Δ (δ from G = A B'^T, SURVEY
+                                    f2) until no swap is accepted for 4096 iterations, then rebuild
+                                    Δ and continue with Δ; 0 = Δ throughout.  Same trajectory. */
 } qap_option;
 qap_status qap_set_option(qap_ctx* ctx, int32_t key, int64_t value);
 /* 1 if the next qap_sa_run uses the tensor-memory engine (QAP_OPT_TENSOR_CORE), else 0. */

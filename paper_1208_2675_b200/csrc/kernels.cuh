@@ -215,6 +215,7 @@ struct ChainArgs {
     int n, ld, M, wmax;
     unsigned long long k0, k_end, seed;
     Sched sch;
+    const unsigned long long* k0_dev;   // if set, k0 is read from device memory (chained launches)
 };
 
 // NFIX > 0: problem size fixed at compile time (layout offsets and loop bounds fold);

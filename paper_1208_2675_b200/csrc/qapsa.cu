@@ -17,6 +17,7 @@
 #include "../../include/qapsa.h"
 #include "kernels.cuh"
 #include "tc_chain.cuh"
+#include "scratch_chain.cuh"
 
 using namespace qapsa;
 
@@ -49,6 +50,8 @@ struct qap_ctx {
     int smem_optin = 0, num_sms = 0;
     bool tc_ok = false;                 // instance fits the tensor-memory engine (tc_chain.cuh)
     int use_tc = 1;
+    int use_scratch = 1;                // high-acceptance phase without Δ (scratch_chain.cuh)
+    unsigned long long* dkout = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     float last_ms = 0.f;
     int last_launches = 0;
@@ -184,7 +187,7 @@ void qap_destroy(qap_ctx* c) {
     void* ptrs[] = {c->dA, c->dB, c->dp0, c->dp, c->dbest, c->dD, c->dperm, c->dDlin, c->drowaddr,
                     c->dqdesc, c->dst, c->dnear_count,
                     c->dnear_k, c->dnear_dec, c->dscratch, c->ens_p0, c->ens_res, c->ens_best,
-                    c->ens_counter};
+                    c->ens_counter, c->dkout};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->ev0) cudaEventDestroy(c->ev0);
@@ -277,6 +280,7 @@ qap_status qap_create(int32_t n, const int32_t* A, const int32_t* B, const int32
     alloc((void**)&c->dnear_k, QAP_NEAR_LOG_CAP * sizeof(unsigned long long));
     alloc((void**)&c->dnear_dec, QAP_NEAR_LOG_CAP);
     alloc((void**)&c->dscratch, 8 * sizeof(long long));
+    alloc((void**)&c->dkout, sizeof(unsigned long long));
     if (st != QAP_OK) {
         qap_destroy(c);
         return st;
@@ -441,11 +445,27 @@ qap_status qap_sa_run(qap_ctx* c, uint64_t k0, uint64_t iters, const qap_schedul
     a.k0 = k0; a.k_end = k0 + iters; a.seed = seed; a.sch = sch;
 
     CU(cudaEventRecord(c->ev0, c->stream));
+    a.k0_dev = nullptr;
     if (tc) {
         a.wmax = c->wmax;
         // compile-time problem size for the BASELINE configurations, generic otherwise
         auto kern = c->n == 100 ? k_sa_tc<100> : c->n == 50 ? k_sa_tc<50> : c->n == 12 ? k_sa_tc<12> : k_sa_tc<0>;
         CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        if (c->use_scratch) {
+            // f2: the high-acceptance phase without Δ, then Δ rebuilt at the iteration reached and
+            // the Δ engine from there (device-side chaining, no host round trip)
+            auto ks = c->n == 100 ? k_sa_scratch<100> : c->n == 50 ? k_sa_scratch<50>
+                    : c->n == 12 ? k_sa_scratch<12> : k_sa_scratch<0>;
+            const int ssm = sc_layout(c->ld).bytes;
+            CU(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, ssm));
+            ks<<<1, TCS_NT, ssm, c->stream>>>(a, c->dkout);
+            CU(cudaGetLastError());
+            const int dt = 256, db = (c->M + dt - 1) / dt;
+            k_delta_init<uint8_t, uint8_t><<<db, dt, 0, c->stream>>>((const uint8_t*)c->dA, (const uint8_t*)c->dB,
+                                                                     c->dp, c->drowaddr, c->n, c->ld, c->M, c->dD);
+            CU(cudaGetLastError());
+            a.k0_dev = c->dkout;
+        }
         kern<<<1, TCK_NT, smem, c->stream>>>(a);
         CU(cudaGetLastError());
     } else {
@@ -458,7 +478,7 @@ qap_status qap_sa_run(qap_ctx* c, uint64_t k0, uint64_t iters, const qap_schedul
     CU(cudaMemcpyAsync(&near_after, c->dnear_count, sizeof near_after, cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
     CU(cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1));
-    c->last_launches = 1;
+    c->last_launches = (tc && c->use_scratch) ? 3 : 1;
     if (out) {
         out->iterations = iters;
         out->accepted = after.accepted - before.accepted;
@@ -676,6 +696,9 @@ qap_status qap_set_option(qap_ctx* c, int32_t key, int64_t value) {
             return QAP_OK;
         case QAP_OPT_TENSOR_CORE:
             c->use_tc = value ? 1 : 0;
+            return QAP_OK;
+        case QAP_OPT_SCRATCH_PHASE:
+            c->use_scratch = value ? 1 : 0;
             return QAP_OK;
         case QAP_OPT_ENSEMBLE_GROUP:
             if (value != 64 && value != 128 && value != 256) return fail(c, QAP_E_INVALID_ARG, "group must be 64, 128 or 256");

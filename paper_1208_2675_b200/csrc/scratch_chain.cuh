@@ -1,0 +1,397 @@
+// scratch_chain.cuh -- the high-acceptance phase of a single chain without Δ: SURVEY §8(f) row f2,
+// "hybrid scratch / Δ mode with an acceptance-rate switch".
+//
+// While swaps are accepted every few iterations, maintaining all of Δ costs an O(N^2) update per
+// accept but each δ is read once or twice before it changes again.  This kernel keeps instead
+//   G[x][f] = sum_k a_xk B[f][p(k)]     (= (A B'^T)[x][p^-1(f)]),   H = G^T,
+// in tensor memory (tensor-memory engine, tc_chain.cuh, reading R10c) and evaluates every
+// candidate's δ from its definition in O(1) (P:46 / S:76 with the sums expanded, R10d):
+//   δ(u,v) = 2 (G_uv + G_vu - D_u - D_v + 2 a_uv B'_uv),   G_uv = (A B'^T)_uv, D_x = G_xx,
+// with G_uv = H[p(v)][u] and G_vu = G[v][p(u)].  An accepted swap changes G by the exact rank-1
+// term -(a_xr - a_xs)(B[f][p(r)] - B[f][p(s)]) (one tcgen05 int8 MMA on [G | H]) and D by
+// D''_v = D_v - dA_v dB_v, D''_r = G_r,p(s) + a_rs B'_rs, D''_s = G_s,p(r) + a_rs B'_rs.
+//
+// The kernel runs from k0 until k_end or until accepts become rare (no accept for
+// TCS_SWITCH_GAP iterations); it then stores p, best_p and the scalars and reports the iteration
+// reached, and qap_sa_run rebuilds Δ (k_delta_init) and continues with the Δ engine (k_sa_tc).
+// Every quantity is an exact integer, so the trajectory is the same whatever the switch point.
+//
+// Threads: 4 lane warps (thread v = TMEM lane v = location v = facility v) and 4 helper warps
+// (MMA issue, thresholds of the next window, digest).
+//
+// Citation keys: P:n = PAPER.md line n, R# = DESIGN.md readings.
+#pragma once
+#include <climits>
+#include <cstdint>
+
+#include "tc_chain.cuh"
+
+namespace qapsa {
+
+constexpr int TCS_NT = 256;
+constexpr uint32_t TCS_COL_G = 0;        // G: TMEM columns [0, 128)
+constexpr uint32_t TCS_COL_H = 128;      // H: TMEM columns [128, 256)
+constexpr uint32_t TCS_COL_L = 256;      // A operand of the update: [dA, -dBf] (K = 32)
+constexpr uint32_t TCS_COLS = 512;
+constexpr uint64_t TCS_SWITCH_GAP = 4096;   // switch to the Δ engine after this many iterations without an accept
+
+struct ScLayout {
+    int a, b, rg, tmp, p, bestp, dg, xch, slots, rec, thm, misc, bytes;
+};
+__host__ __device__ inline ScLayout sc_layout(int ld) {
+    ScLayout L;
+    int o = 0;
+    L.a = o;     o += 128 * ld;
+    L.b = o;     o += 128 * ld;
+    o = (o + 1023) & ~1023;
+    L.rg = o;    o += 256 * 32;                 // [G | H] update B operand, K-major canonical (SBO 256)
+    L.tmp = o;   o += 2 * 128 * 128;            // init only: A, C canonical (SBO 1024)
+    L.p = o;     o += 128 * 2;
+    L.bestp = o; o += 128 * 2;
+    L.dg = o;    o += 128 * 4;                  // D_x
+    L.xch = o;   o += 4 * 128 * 4;              // G[u_i][p(v)] by window row i and location v
+    L.slots = o; o += 2 * 4 * 16;
+    L.rec = o;   o += 32;
+    L.thm = o;   o += TCK_TH * 8;
+    L.misc = o;  o += 64;                       // mbarrier | TMEM base
+    L.bytes = o;
+    return L;
+}
+
+template <int NFIX>
+__global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, unsigned long long* k_out) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int n = NFIX ? NFIX : a.n;
+    const int ld = NFIX ? row_stride(NFIX, true) : a.ld;
+    const int M = n * (n - 1) / 2;
+    const ScLayout L = sc_layout(ld);
+    uint8_t* As = smem + L.a;
+    uint8_t* Bs = smem + L.b;
+    uint8_t* Rg = smem + L.rg;
+    uint16_t* p = reinterpret_cast<uint16_t*>(smem + L.p);
+    uint16_t* best_p = reinterpret_cast<uint16_t*>(smem + L.bestp);
+    int* Dg = reinterpret_cast<int*>(smem + L.dg);
+    int* xch = reinterpret_cast<int*>(smem + L.xch);
+    int4* slots = reinterpret_cast<int4*>(smem + L.slots);
+    int* rec = reinterpret_cast<int*>(smem + L.rec);
+    float2* thm = reinterpret_cast<float2*>(smem + L.thm);
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + L.misc);          // G|H update done
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.misc + 8);
+    uint64_t* mbar_t = reinterpret_cast<uint64_t*>(smem + L.misc + 16);   // next-window thresholds written
+    const bool lanew = warp < 4;
+    const uint32_t quad_lane = (uint32_t)(32 * (warp & 3)) << 16;
+    const int v = t & 127;
+    const bool vin = v < n;
+
+    // ---------------- load the chain state; G and H on the tensor cores ----------------
+    copy_words(As, a.A, n * ld, t, TCS_NT);
+    copy_words(Bs, a.B, n * ld, t, TCS_NT);
+    for (int i = t; i < n; i += TCS_NT) {
+        p[i] = (uint16_t)a.p[i];
+        best_p[i] = (uint16_t)a.best_p[i];
+    }
+    for (int i = t; i < 256 * 32 / 16; i += TCS_NT) reinterpret_cast<uint4*>(Rg)[i] = make_uint4(0, 0, 0, 0);
+    if (warp == 0) tc::tmem_alloc(tmem_slot, TCS_COLS);
+    if (t == 0) { tc::mbar_init(mbar, 1); tc::mbar_init(mbar_t, 4); }
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tm = *tmem_slot;
+    {
+        uint8_t* Ac = smem + L.tmp;
+        uint8_t* Cc = Ac + 128 * 128;
+        for (int idx = t; idx < 128 * 128; idx += TCS_NT) {
+            const int x = idx >> 7, kk = idx & 127;
+            const bool in = x < n && kk < n;
+            Ac[cofs(x, kk)] = in ? As[x * ld + kk] : (uint8_t)0;
+            Cc[cofs(x, kk)] = in ? Bs[x * ld + p[kk]] : (uint8_t)0;
+        }
+        if (lanew) {
+            tc::tmem_st4(tm + quad_lane + TCS_COL_L, 0u, 0u, 0u, 0u);
+            tc::tmem_st4(tm + quad_lane + TCS_COL_L + 4, 0u, 0u, 0u, 0u);
+            tc::tmem_wait_st();
+        }
+        tc::fence_proxy_async();
+        tc::fence_before_sync();
+        __syncthreads();
+        if (t == 0) {                            // G = A C^T, H = C A^T
+            tc::fence_after_sync();
+            const uint32_t id = tc::idesc_i8(128, 128, true);
+            for (int kc = 0; kc < 4; ++kc)
+                tc::mma_i8(tm + TCS_COL_G, tc::smem_desc(tc::smem_u32(Ac) + 256 * kc, 128, 1024),
+                           tc::smem_desc(tc::smem_u32(Cc) + 256 * kc, 128, 1024), id, kc > 0);
+            for (int kc = 0; kc < 4; ++kc)
+                tc::mma_i8(tm + TCS_COL_H, tc::smem_desc(tc::smem_u32(Cc) + 256 * kc, 128, 1024),
+                           tc::smem_desc(tc::smem_u32(Ac) + 256 * kc, 128, 1024), id, kc > 0);
+            tc::mma_commit(mbar);
+        }
+    }
+    int px = vin ? p[v] : 0;                     // p(v)
+    int qv = 0;                                  // p^-1(v)
+    for (int i = 0; i < n; ++i) qv = (p[i] == v) ? i : qv;
+    if (lanew) {
+        int dgv = 0;
+        if (vin)
+            for (int kk = 0; kk < n; ++kk) dgv += (int)As[v * ld + kk] * (int)Bs[px * ld + p[kk]];
+        Dg[v] = dgv;
+    }
+    tc::mbar_wait(mbar, 0);
+    uint32_t ph = 1;
+    tc::fence_after_sync();
+    __syncthreads();
+
+    const Sched sch = a.sch;
+    const uint64_t seed = a.seed, k_end = a.k_end;
+    const NearSink sink{a.near_count, a.near_k, a.near_dec, a.near_cap};
+    int64_t cost = a.st->cost, best = a.st->best_cost;
+    uint64_t digest = a.st->digest;
+    uint64_t k = a.k0, accepted = 0, k_last = a.k0;
+    int u0, v0;
+    tri_pair(n, (int)(k % (uint64_t)M), &u0, &v0);
+    const int wmax = a.wmax;
+    int W = wmax;
+    int parity = 0;
+    int rejI = rej_bound(sch, k);
+    uint64_t pk = ~0ull;                         // window whose thresholds are in thm
+    int pn = 0;
+    const uint32_t id_gh = tc::idesc_i8(128, 256, true);
+#ifdef QAPSA_PHASE_TIMERS
+    long long tacc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+#endif
+
+  if (lanew) {
+    uint32_t ph_t = 0;                           // phase of the thresholds mbarrier (one per accept)
+    while (k < k_end && k - k_last < TCS_SWITCH_GAP) {
+        // ---------------- window: rows u0 .. u0+R-1 (R <= 4) ----------------
+        TCT_MARK(pt0, u0 + v0);
+        const int R = win_rows<4>(n, u0), L0 = n - v0, m1 = n - 1 - u0;
+        int Wl = win_f(R, L0, m1);
+        if (W < Wl) Wl = W;
+        {
+            const uint64_t remaining = k_end - k;
+            if ((uint64_t)Wl > remaining) Wl = (int)remaining;
+        }
+        int rb[4], rf[4], pu[4];
+        {
+            int f = 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                rf[i] = i == 0 ? v0 : u0 + i + 1;
+                rb[i] = f - rf[i];
+                f += i == 0 ? L0 : m1 - i;
+                pu[i] = p[min(u0 + i, n - 1)];
+            }
+        }
+        uint32_t gv[4], hf[4];                   // G[v][p(u_i)] (location lane v), H[f][u_i] (facility lane f = v)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) tc::tmem_ld1(tm + quad_lane + TCS_COL_G + (uint32_t)pu[i], gv[i]);
+        tc::tmem_ld4(tm + quad_lane + TCS_COL_H + (uint32_t)u0, hf);
+        tc::tmem_wait_ld();
+        if (vin) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) xch[i * 128 + qv] = (int)hf[i];   // G[u_i][v] to location p^-1(v)
+        }
+        TCT_ACC(0, pt0, u0);
+        group_sync(3, 128);                      // exchange
+        TCT_ACC(1, pt0, xch[v]);
+        int4* sl = slots + parity * 4;
+        unsigned acc_mask = 0, near_mask = 0;
+        const int dv = Dg[v];
+        unsigned need = 0;
+        int dd[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int u = min(u0 + i, n - 1);
+            const int guv = xch[i * 128 + v];                   // G_uv = (A B'^T)[u][v]
+            const int auv = As[u * ld + v], buv = Bs[pu[i] * ld + px];
+            dd[i] = 2 * (guv + (int)gv[i] - Dg[u] - dv + 2 * auv * buv);   // δ(u, v) (R10d)
+            const int o = rb[i] + v;
+            const bool ex = i < R && v >= rf[i] && vin && o < Wl;
+            acc_mask |= (unsigned)(ex && dd[i] <= 0) << i;      // δ <= 0 (R5)
+            need |= (unsigned)(ex && dd[i] > 0 && dd[i] <= rejI) << i;
+        }
+        const bool prepared = pk == k;           // the first window after an accept
+        if (__any_sync(0xffffffffu, need != 0)) {
+            const int pnk = prepared ? pn : 0;
+            if (prepared) tc::mbar_wait(mbar_t, ph_t);   // the helpers' thresholds are written
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                if ((need >> i) & 1u) {
+                    const int o = rb[i] + v;
+                    float th, m;
+                    if (o < pnk) { const float2 q = thm[o]; th = q.x; m = q.y; }
+                    else theta_of(sch, seed, k + (uint64_t)o, &th, &m);
+                    const float df = (float)dd[i];
+                    bool ac = df < th - m;
+                    if (!ac && !(df > th + m)) {  // inside the margin: exact double test (R16)
+                        const int x = tc_exact(dd[i], k + (uint64_t)o, sch, seed);
+                        ac = x & 1;
+                        near_mask |= (unsigned)((x >> 1) & 1) << i;
+                    }
+                    acc_mask |= (unsigned)ac << i;
+                }
+            }
+        }
+        if (prepared) ph_t ^= 1;                 // one thresholds phase per accept
+        int best_o = INT_MAX, best_d = 0, best_rs = 0;
+#pragma unroll
+        for (int i = 3; i >= 0; --i) {
+            const bool ac = (acc_mask >> i) & 1u;
+            best_o = ac ? rb[i] + v : best_o;
+            best_d = ac ? dd[i] : best_d;
+            best_rs = ac ? ((u0 + i) | (v << 8) | (pu[i] << 16) | (px << 24)) : best_rs;
+        }
+        {
+            const int wmin = __reduce_min_sync(0xffffffffu, best_o);
+            if (best_o == wmin && (wmin != INT_MAX || lane == 0)) sl[warp] = make_int4(best_o, best_d, best_rs, 0);
+        }
+        TCT_ACC(2, pt0, acc_mask);
+        group_sync(4, 128);                      // window decision
+        const int tv = lane < 4 ? sl[lane].x : INT_MAX;
+        const int j = __reduce_min_sync(0xffffffffu, tv);
+        TCT_MARK(pt1, j);
+        parity ^= 1;
+        const int consumed = (j == INT_MAX) ? Wl : j + 1;
+        if (near_mask) {                         // R16: log near ties of consumed iterations
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int o = rb[i] + v;
+                if (((near_mask >> i) & 1u) && o < consumed) {
+                    const unsigned int e = atomicAdd(sink.count, 1u);
+                    if ((int)e < sink.cap) {
+                        sink.ks[e] = (unsigned long long)(k + (uint64_t)o);
+                        sink.dec[e] = (unsigned char)((acc_mask >> i) & 1u);
+                    }
+                }
+            }
+        }
+        if (j == INT_MAX) {
+            k += (uint64_t)Wl;
+            win_advance<4>(n, u0, v0, Wl, &u0, &v0);
+            W = min(2 * W, wmax);
+            rejI = rej_bound(sch, k);
+            continue;
+        }
+        const unsigned bw = __ballot_sync(0xffffffffu, tv == j);
+        const int4 win = sl[__ffs(bw) - 1];
+        const int dw = win.y;
+        const int r = win.z & 0xFF, s = (win.z >> 8) & 0xFF;
+        const int pr = (win.z >> 16) & 0xFF, ps = (int)((unsigned)win.z >> 24);
+        const uint64_t kacc = k + (uint64_t)j;
+        // ---------------- stage: the G|H update operands, D'' ----------------
+        int arv = 0, asv = 0, brv = 0, bsv = 0, bfr = 0, bfs = 0;
+        if (vin) {
+            arv = As[r * ld + v]; asv = As[s * ld + v];
+            brv = Bs[pr * ld + px]; bsv = Bs[ps * ld + px];
+            bfr = Bs[pr * ld + v]; bfs = Bs[ps * ld + v];
+        }
+        const int dA = arv - asv, dB = brv - bsv, dBf = bfr - bfs;
+        uint32_t gps, gpr;                       // G[v][p(s)], G[v][p(r)] (pre-update)
+        tc::tmem_ld1(tm + quad_lane + TCS_COL_G + (uint32_t)ps, gps);
+        tc::tmem_ld1(tm + quad_lane + TCS_COL_G + (uint32_t)pr, gpr);
+        tc::tmem_st1(tm + quad_lane + TCS_COL_L, b8(dA) | (b8(-dBf) << 8));
+        const int ro = (v >> 3) * 256 + (v & 7) * 16;
+        *reinterpret_cast<uint32_t*>(Rg + ro) = b8(-dBf);               // G rows: facility v
+        *reinterpret_cast<uint32_t*>(Rg + 4096 + ro) = b8(dA) << 8;    // H rows: location v
+        const int ars = As[r * ld + s], brs = Bs[pr * ld + ps];
+        int nu0, nv0;                            // next window: cursor after (r, s)
+        next_pair(n, r, s, &nu0, &nv0);
+        const int Wn = max(64, min(wmax, round_up32(8 * (j + 1))));
+        int Wln = win_total<4>(n, nu0, nv0);
+        if (Wn < Wln) Wln = Wn;
+        if (kacc + 1 + (uint64_t)Wln > k_end) Wln = (int)(k_end - kacc - 1);
+        const int npn = Wln < TCK_TH ? Wln : TCK_TH;
+        if (t == 0) {                            // the accept, for the helper warps
+            rec[0] = r; rec[1] = s;
+            rec[2] = (int)(uint32_t)kacc; rec[3] = (int)(uint32_t)(kacc >> 32);
+            rec[4] = npn;
+        }
+        tc::tmem_wait_ld();
+        const int dnew = (v == r) ? (int)gps + ars * brs : (v == s) ? (int)gpr + ars * brs : dv - dA * dB;
+        TCT_ACC(3, pt1, dnew);
+        tc::fence_proxy_async();
+        tc::tmem_wait_st();
+        tc::fence_before_sync();
+        group_sync(1, TCS_NT);                   // operands staged; the helpers take the accept
+        TCT_ACC(4, pt1, p[0]);
+        if (t == 0) {
+            tc::fence_after_sync();
+            // [G | H] (256 columns) += [dA, -dBf] [[-dBf, 0]; [0, dA]]^T
+            tc::mma_i8_ts(tm + TCS_COL_G, tm + TCS_COL_L, tc::smem_desc(tc::smem_u32(Rg), 128, 256), id_gh, true);
+            tc::mma_commit(mbar);
+        }
+        if (vin) Dg[v] = dnew;
+        if (v == r) p[v] = (uint16_t)ps;
+        if (v == s) p[v] = (uint16_t)pr;
+        cost += dw;
+        const bool improved = cost < best;
+        if (improved) {
+            best = cost;
+            if (vin) best_p[v] = (uint16_t)((v == r) ? ps : (v == s) ? pr : px);
+        }
+        tc::mbar_wait(mbar, ph);                 // G, H updated before the next window reads them
+        ph ^= 1;
+        tc::fence_after_sync();
+        TCT_ACC(5, pt1, ph);
+        group_sync(2, 128);                      // D, p complete
+        TCT_ACC(6, pt1, Dg[0]);
+        TCT_ACC(7, pt0, Dg[1]);
+        px = (v == r) ? ps : (v == s) ? pr : px;
+        qv = (v == pr) ? s : (v == ps) ? r : qv;
+        pk = kacc + 1;
+        pn = npn;
+        u0 = nu0;
+        v0 = nv0;
+        W = Wn;
+        ++accepted;
+        k = kacc + 1;
+        k_last = k;
+        rejI = rej_bound(sch, k);
+    }
+    if (t == 0) rec[0] = -1;
+    group_sync(1, TCS_NT);                       // release the helpers
+  } else {
+    // ---------------- helper warps: thresholds of the window after each accept, digest ----------------
+    while (true) {
+        group_sync(1, TCS_NT);
+        const int r = rec[0];
+        if (r < 0) break;
+        const int s = rec[1], npn = rec[4];
+        const uint64_t kacc = (uint64_t)(uint32_t)rec[2] | ((uint64_t)(uint32_t)rec[3] << 32);
+        for (int o = v; o < npn; o += 128) {
+            float th, m;
+            theta_of(sch, seed, kacc + 1 + (uint64_t)o, &th, &m);
+            thm[o] = make_float2(th, m);
+        }
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(mbar_t);  // 4 helper warps: the thresholds are written
+        if (t == 128) digest = digest_step(digest, kacc, r, s);
+    }
+  }
+
+    // ---------------- write the chain state back (Δ is rebuilt by the caller) ----------------
+#ifdef QAPSA_PHASE_TIMERS
+    if (lane == 0)
+        for (int i = 0; i < 12; ++i) atomicAdd(&g_phase_cycles[16 * warp + i], (unsigned long long)tacc[i]);
+    if (t == 0) { atomicAdd(&g_phase_cycles[127], accepted); }
+#endif
+    __syncthreads();
+    for (int i = t; i < n; i += TCS_NT) {
+        a.p[i] = p[i];
+        a.best_p[i] = best_p[i];
+    }
+    if (t == 0) {
+        a.st->cost = cost;
+        a.st->best_cost = best;
+        a.st->accepted += accepted;
+        *k_out = k;
+    }
+    if (t == 128) a.st->digest = digest;
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    if (warp == 0) tc::tmem_dealloc(tm, TCS_COLS);
+}
+
+}  // namespace qapsa

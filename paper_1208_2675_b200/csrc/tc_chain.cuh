@@ -118,13 +118,16 @@ __device__ __forceinline__ uint32_t pack8(int a, int b, int c, int d) {
 __device__ __forceinline__ int win_f(int i, int L0, int m1) {   // f_i for i >= 1
     return L0 + (i - 1) * m1 - (((i - 1) * i) >> 1);
 }
-__device__ __forceinline__ int win_rows(int n, int u0) { return min(TCK_WR, n - 1 - u0); }
+template <int RMAX = TCK_WR>
+__device__ __forceinline__ int win_rows(int n, int u0) { return min(RMAX, n - 1 - u0); }
+template <int RMAX = TCK_WR>
 __device__ __forceinline__ int win_total(int n, int u0, int v0) {
-    return win_f(win_rows(n, u0), n - v0, n - 1 - u0);
+    return win_f(win_rows<RMAX>(n, u0), n - v0, n - 1 - u0);
 }
 // cursor after the first x candidates of the window (0 < x <= total)
+template <int RMAX = TCK_WR>
 __device__ __forceinline__ void win_advance(int n, int u0, int v0, int x, int* nu, int* nv) {
-    const int R = win_rows(n, u0), L0 = n - v0, m1 = n - 1 - u0;
+    const int R = win_rows<RMAX>(n, u0), L0 = n - v0, m1 = n - 1 - u0;
     if (x >= win_f(R, L0, m1)) {
         const int u = u0 + R;
         if (u >= n - 1) { *nu = 0; *nv = 1; }
@@ -134,7 +137,7 @@ __device__ __forceinline__ void win_advance(int n, int u0, int v0, int x, int* n
     if (x < L0) { *nu = u0; *nv = v0 + x; return; }
     int i = 1, f = L0;                           // row i >= 1 holding offset x
 #pragma unroll
-    for (int e = 2; e < TCK_WR; ++e) {
+    for (int e = 2; e < RMAX; ++e) {
         const int fe = win_f(e, L0, m1);
         if (e < R && x >= fe) { i = e; f = fe; }
     }
@@ -268,7 +271,7 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
     const NearSink sink{a.near_count, a.near_k, a.near_dec, a.near_cap};
     int64_t cost = a.st->cost, best = a.st->best_cost;
     uint64_t digest = a.st->digest;
-    uint64_t k = a.k0, accepted = 0;
+    uint64_t k = a.k0_dev ? *a.k0_dev : a.k0, accepted = 0;
     int u0, v0;
     tri_pair(n, (int)(k % (uint64_t)M), &u0, &v0);
     const int wmax = a.wmax;

@@ -23,6 +23,7 @@ STATUS = {0: "QAP_OK", 1: "QAP_E_INVALID_ARG", 2: "QAP_E_DIMENSION", 3: "QAP_E_U
 QAP_COOL_GEOMETRIC, QAP_COOL_LUNDY_MEES = 0, 1
 QAP_OPT_WINDOW_MAX, QAP_OPT_THREADS, QAP_OPT_FORCE_GLOBAL_DELTA, QAP_OPT_ENSEMBLE_GROUP = 1, 2, 3, 4
 QAP_OPT_TENSOR_CORE = 5
+QAP_OPT_SCRATCH_PHASE = 6
 QAP_NEAR_LOG_CAP = 1024
 
 # Every symbol include/qapsa.h declares (checked by tests/test_abi.py).

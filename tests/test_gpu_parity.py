@@ -17,8 +17,11 @@ if not torch.cuda.is_available():
 
 
 TC = Q.QAP_OPT_TENSOR_CORE
-# both single-chain engines: Δ in tensor memory (default where eligible) and Δ in shared memory
-ENGINES = [pytest.param(1, id="tmem"), pytest.param(0, id="smem")]
+SCR = Q.QAP_OPT_SCRATCH_PHASE
+# the single-chain engines: tensor memory with the Δ-free high-acceptance phase (default where
+# eligible), tensor memory with Δ throughout, shared memory
+ENGINES = [pytest.param([(TC, 1), (SCR, 1)], id="tmem"), pytest.param([(TC, 1), (SCR, 0)], id="tmem_delta"),
+           pytest.param([(TC, 0)], id="smem")]
 
 
 def _sched(s: O.Schedule):
@@ -109,7 +112,7 @@ def test_reset_restores_p0_and_perm():
 def test_config1_full_bit_exact(engine):
     A, B, p0, cfg = config(1)
     sch = O.geometric_schedule_for(A, B, p0, cfg["iters"])
-    g, acc = _compare_run(A, B, p0, cfg["iters"], sch, opts=[(TC, engine)])
+    g, acc = _compare_run(A, B, p0, cfg["iters"], sch, opts=engine)
     assert acc > 100
 
 
@@ -117,7 +120,7 @@ def test_config1_full_bit_exact(engine):
 def test_config2_full_bit_exact(engine):
     A, B, p0, cfg = config(2)
     sch = O.geometric_schedule_for(A, B, p0, cfg["iters"])
-    _compare_run(A, B, p0, cfg["iters"], sch, mode=O.MODE_SCRATCH, opts=[(TC, engine)])
+    _compare_run(A, B, p0, cfg["iters"], sch, mode=O.MODE_SCRATCH, opts=engine)
 
 
 def test_engine_selection():
@@ -156,12 +159,13 @@ def test_tmem_engine_full_range_values(n, seed):
     assert acc > 100
 
 
+@pytest.mark.parametrize("scratch", [1, 0])
 @pytest.mark.parametrize("wmax", [32, 64, 256, 1024])
-def test_tmem_window_invariance(wmax):
+def test_tmem_window_invariance(wmax, scratch):
     A, B = taixxa(100, 77)
     p0 = start_perm(100, 5, 0)
     sch = O.geometric_schedule_for(A, B, p0, 200000)
-    _compare_run(A, B, p0, 200000, sch, opts=[(Q.QAP_OPT_WINDOW_MAX, wmax)])
+    _compare_run(A, B, p0, 200000, sch, opts=[(Q.QAP_OPT_WINDOW_MAX, wmax), (SCR, scratch)])
 
 
 @pytest.mark.parametrize("threads,wmax", [(256, 32), (512, 128), (1024, 1024), (1024, 64),
@@ -181,7 +185,7 @@ def test_resume_split_calls(engine):
     p0 = start_perm(37, 9, 0)
     I = 300000
     sch = O.geometric_schedule_for(A, B, p0, I)
-    _compare_run(A, B, p0, I, sch, k_splits=[0, 1, 999, 1000, 123457, I], opts=[(TC, engine)])
+    _compare_run(A, B, p0, I, sch, k_splits=[0, 1, 999, 1000, 123457, I], opts=engine)
 
 
 def test_global_delta_variant():
@@ -198,7 +202,7 @@ def test_lundy_mees_schedule(engine):
     p0 = start_perm(30, 1, 0)
     g = O.geometric_schedule_for(A, B, p0, 100000)
     sch = O.Schedule(O.COOL_LUNDY_MEES, g.t0, g.tf, 100000)
-    _compare_run(A, B, p0, 100000, sch, opts=[(TC, engine)])
+    _compare_run(A, B, p0, 100000, sch, opts=engine)
 
 
 @pytest.mark.parametrize("engine", ENGINES)
@@ -208,7 +212,7 @@ def test_tiny_instances_window_wraps(n, engine):
     A, B = taixxa(n, 40 + n)
     p0 = start_perm(n, n, 0)
     sch = O.geometric_schedule_for(A, B, p0, 20000)
-    _compare_run(A, B, p0, 20000, sch, opts=[(TC, engine)])
+    _compare_run(A, B, p0, 20000, sch, opts=engine)
 
 
 @pytest.mark.parametrize("engine", ENGINES)
@@ -218,7 +222,7 @@ def test_all_zero_flow_every_iteration_accepts(engine):
     A = np.zeros((n, n), np.int32)
     p0 = start_perm(n, 1, 0)
     sch = O.Schedule(O.COOL_GEOMETRIC, 1.0, 0.1, 5000)
-    g, acc = _compare_run(A, B, p0, 5000, sch, opts=[(TC, engine)])
+    g, acc = _compare_run(A, B, p0, 5000, sch, opts=engine)
     assert acc == 5000 and g["cost"] == 0
 
 
@@ -228,7 +232,8 @@ def test_single_iteration_and_tail_of_schedule(engine):
     p0 = start_perm(25, 2, 0)
     sch = O.geometric_schedule_for(A, B, p0, 10**6)
     with Q.Solver(A, B, p0) as s:
-        s.set_option(TC, engine)
+        for kv in engine:
+            s.set_option(*kv)
         s.delta_init()
         g = s.run(10**6 - 1, 1, _sched(sch), 7)
         _, _, D = s.state()
