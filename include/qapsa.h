@@ -198,6 +198,11 @@ int32_t qap_uses_tensor_core(const qap_ctx* ctx);
 /* Device time in milliseconds of the last qap_sa_run kernel (CUDA events
  * on the context stream), and the number of kernels the last call launched. */
 qap_status qap_last_kernel_time(qap_ctx* ctx, float* ms, int32_t* launches);
+/* The last qap_sa_run's scratch phase (QAP_OPT_SCRATCH_PHASE): device time in milliseconds
+ * (CUDA events around its kernel; the rest of qap_last_kernel_time is the Δ rebuild and the Δ
+ * engine), the iteration it reached (where the Δ engine took over) and the swaps it accepted.
+ * All zero if it did not run.  Any argument may be NULL. */
+qap_status qap_last_scratch_time(qap_ctx* ctx, float* ms, uint64_t* k_reached, uint64_t* accepted);
 
 const char* qap_status_str(qap_status st);
 /* Last error message on ctx ("" if none); static string if ctx is NULL. */

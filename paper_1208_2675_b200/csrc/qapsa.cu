@@ -52,7 +52,9 @@ struct qap_ctx {
     int use_tc = 1;
     int use_scratch = 1;                // high-acceptance phase without Δ (scratch_chain.cuh)
     unsigned long long* dkout = nullptr;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, evm = nullptr;   // evm: after the scratch phase
+    float last_scratch_ms = 0.f;
+    unsigned long long last_scratch[2] = {0, 0};   // iteration reached, accepted swaps
     float last_ms = 0.f;
     int last_launches = 0;
 };
@@ -192,6 +194,7 @@ void qap_destroy(qap_ctx* c) {
         if (p) cudaFree(p);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
+    if (c->evm) cudaEventDestroy(c->evm);
     delete c;
 }
 
@@ -280,12 +283,13 @@ qap_status qap_create(int32_t n, const int32_t* A, const int32_t* B, const int32
     alloc((void**)&c->dnear_k, QAP_NEAR_LOG_CAP * sizeof(unsigned long long));
     alloc((void**)&c->dnear_dec, QAP_NEAR_LOG_CAP);
     alloc((void**)&c->dscratch, 8 * sizeof(long long));
-    alloc((void**)&c->dkout, sizeof(unsigned long long));
+    alloc((void**)&c->dkout, 2 * sizeof(unsigned long long));
     if (st != QAP_OK) {
         qap_destroy(c);
         return st;
     }
-    if (cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess) {
+    if (cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
+        cudaEventCreate(&c->evm) != cudaSuccess) {
         qap_destroy(c);
         return fail(nullptr, QAP_E_CUDA, "cudaEventCreate failed");
     }
@@ -460,6 +464,7 @@ qap_status qap_sa_run(qap_ctx* c, uint64_t k0, uint64_t iters, const qap_schedul
             CU(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, ssm));
             ks<<<1, TCS_NT, ssm, c->stream>>>(a, c->dkout);
             CU(cudaGetLastError());
+            CU(cudaEventRecord(c->evm, c->stream));
             const int dt = 256, db = (c->M + dt - 1) / dt;
             k_delta_init<uint8_t, uint8_t><<<db, dt, 0, c->stream>>>((const uint8_t*)c->dA, (const uint8_t*)c->dB,
                                                                      c->dp, c->drowaddr, c->n, c->ld, c->M, c->dD);
@@ -478,6 +483,12 @@ qap_status qap_sa_run(qap_ctx* c, uint64_t k0, uint64_t iters, const qap_schedul
     CU(cudaMemcpyAsync(&near_after, c->dnear_count, sizeof near_after, cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
     CU(cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1));
+    c->last_scratch_ms = 0.f;
+    c->last_scratch[0] = c->last_scratch[1] = 0;
+    if (tc && c->use_scratch) {
+        CU(cudaEventElapsedTime(&c->last_scratch_ms, c->ev0, c->evm));
+        CU(cudaMemcpy(c->last_scratch, c->dkout, sizeof c->last_scratch, cudaMemcpyDeviceToHost));
+    }
     c->last_launches = (tc && c->use_scratch) ? 3 : 1;
     if (out) {
         out->iterations = iters;
@@ -709,6 +720,14 @@ qap_status qap_set_option(qap_ctx* c, int32_t key, int64_t value) {
 }
 
 int32_t qap_uses_tensor_core(const qap_ctx* c) { return (c && use_tc_engine(c)) ? 1 : 0; }
+
+qap_status qap_last_scratch_time(qap_ctx* c, float* ms, uint64_t* k_reached, uint64_t* accepted) {
+    CHECK_CTX(c);
+    if (ms) *ms = c->last_scratch_ms;
+    if (k_reached) *k_reached = c->last_scratch[0];
+    if (accepted) *accepted = c->last_scratch[1];
+    return QAP_OK;
+}
 
 qap_status qap_last_kernel_time(qap_ctx* c, float* ms, int32_t* launches) {
     CHECK_CTX(c);

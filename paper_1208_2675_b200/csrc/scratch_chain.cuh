@@ -385,7 +385,8 @@ __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, uns
         a.st->cost = cost;
         a.st->best_cost = best;
         a.st->accepted += accepted;
-        *k_out = k;
+        k_out[0] = k;                            // iteration reached (the Δ engine starts here)
+        k_out[1] = accepted;                     // swaps accepted in this phase
     }
     if (t == 128) a.st->digest = digest;
     tc::fence_before_sync();

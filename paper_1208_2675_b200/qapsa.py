@@ -29,7 +29,8 @@ QAP_NEAR_LOG_CAP = 1024
 # Every symbol include/qapsa.h declares (checked by tests/test_abi.py).
 EXPORTS = ("qap_create", "qap_destroy", "qap_reset", "qap_delta_init", "qap_sa_run", "qap_cost",
            "qap_get_state", "qap_get_near_ties", "qap_schedule_bounds", "qap_ensemble_run",
-           "qap_set_option", "qap_uses_tensor_core", "qap_last_kernel_time", "qap_status_str",
+           "qap_set_option", "qap_uses_tensor_core", "qap_last_kernel_time", "qap_last_scratch_time",
+           "qap_status_str",
            "qap_last_error", "qap_version")
 
 
@@ -90,6 +91,7 @@ def lib(build_if_missing: bool = True):
                                    C.POINTER(qap_chain_result)]
     L.qap_set_option.argtypes = [vp, C.c_int32, C.c_int64]
     L.qap_last_kernel_time.argtypes = [vp, C.POINTER(C.c_float), i32p]
+    L.qap_last_scratch_time.argtypes = [vp, C.POINTER(C.c_float), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
     L.qap_status_str.argtypes = [C.c_int]
     L.qap_status_str.restype = C.c_char_p
     L.qap_last_error.argtypes = [vp]
@@ -228,6 +230,13 @@ def qap_uses_tensor_core(ctx) -> bool:
     return bool(lib().qap_uses_tensor_core(ctx))
 
 
+def qap_last_scratch_time(ctx):
+    """(ms, iteration reached, swaps accepted) of the last run's scratch phase."""
+    ms, kr, acc = C.c_float(), C.c_uint64(), C.c_uint64()
+    _check(lib().qap_last_scratch_time(ctx, C.byref(ms), C.byref(kr), C.byref(acc)), ctx)
+    return ms.value, kr.value, acc.value
+
+
 def qap_last_kernel_time(ctx):
     ms, nl = C.c_float(), C.c_int32()
     _check(lib().qap_last_kernel_time(ctx, C.byref(ms), C.byref(nl)), ctx)
@@ -306,3 +315,6 @@ class Solver:
 
     def last_kernel_time(self):
         return qap_last_kernel_time(self.ctx)
+
+    def last_scratch_time(self):
+        return qap_last_scratch_time(self.ctx)

@@ -15,8 +15,12 @@ timeout 300 $CMD > $OUT/plain.log 2>&1 && \
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file $OUT/launches_$TAG.csv $CMD > $OUT/ncu_launch.log 2>&1
 echo "launches rc=$?" >> $OUT/ncu_launch.log
-# full capture of the dominant kernel (tensor-memory engine) on a short run of config 3
+# full captures: the scratch phase (dominant) on config 3's hot start, the Δ engine on its tail
 timeout 120 python tools/run_cfg3.py 2e5 > $OUT/prof_plain.log 2>&1 && \
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_sa_tc -c 1 \
-    -o $OUT/prof_sa_tc_$TAG python tools/run_cfg3.py 2e5 > $OUT/ncu_full.log 2>&1
-echo "full rc=$?" >> $OUT/ncu_full.log
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_sa_scratch -c 1 \
+    -o $OUT/prof_sa_scratch_$TAG python tools/run_cfg3.py 2e5 > $OUT/ncu_full.log 2>&1
+echo "full scratch rc=$?" >> $OUT/ncu_full.log
+timeout 120 python tools/run_cfg3.py 2e6 3e7 > $OUT/prof_plain_tc.log 2>&1 && \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sa_tc -c 1 \
+    -o $OUT/prof_sa_tc_$TAG python tools/run_cfg3.py 2e6 3e7 > $OUT/ncu_full_tc.log 2>&1
+echo "full tc rc=$?" >> $OUT/ncu_full_tc.log
