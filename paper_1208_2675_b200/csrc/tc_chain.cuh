@@ -50,7 +50,7 @@ namespace qapsa {
 
 constexpr int TCK_NT = 256;              // 8 warps: 4 lane warps (thread v <-> TMEM lane v), 4 helpers
 constexpr int TCK_NW = 8;                // warps: window slots
-constexpr int TCK_WR = 8;                // window rows (4 per half of the CTA)
+constexpr int TCK_WR = 16;               // window rows (8 per half of the CTA, two tcgen05.ld of 4 columns)
 constexpr int TCK_TH = 256;              // thresholds prepared ahead per window (offsets < TCK_TH)
 constexpr uint32_t TCK_COL_G = 128;      // G: TMEM columns [128, 256)
 constexpr uint32_t TCK_COL_H = 256;      // H = G^T: TMEM columns [256, 384)
@@ -302,19 +302,24 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
         }
         int4* sl = slots + parity * TCK_NW;
         unsigned acc_mask = 0, near_mask = 0;
-        const int h4 = 4 * (warp >> 2);          // this warp's window rows: u0 + h4 .. u0 + h4 + 3
-        int rb[4], rf[4];                        // offset base (f_i - first_i) and first column of its rows
+        // this warp's window rows: u0 + hb .. u0 + hb + 7 (two groups of 4), hb = 8 (warp >> 2)
+        const int hb = 8 * (warp >> 2);
+        int rb[8], rf[8];                        // offset base (f_i - first_i) and first column of its rows
         {
-            int f = h4 == 0 ? 0 : win_f(h4, L0, m1);
+            int f = hb == 0 ? 0 : win_f(hb, L0, m1);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int ii = h4 + i;
+            for (int i = 0; i < 8; ++i) {
+                const int ii = hb + i;
                 rf[i] = ii == 0 ? v0 : u0 + ii + 1;
                 rb[i] = f - rf[i];
                 f += ii == 0 ? L0 : m1 - ii;
             }
         }
-        if (h4 < R && rb[0] + rf[0] < Wl) {      // warp-uniform: the rows hold candidates
+        int best_o = INT_MAX, best_d = 0, best_rs = 0;
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+            const int h4 = hb + 4 * g;
+            if (!(h4 < R && rb[4 * g] + rf[4 * g] < Wl)) continue;   // warp-uniform: no candidates
             uint32_t dd[4];
             tc::tmem_ld4(tm + quad_lane + (uint32_t)(u0 + h4), dd);   // Δ_{u0+h4+i, v} (columns u0+h4 ..)
             int pu[4];                           // p(row): carried to the accepted slot
@@ -328,13 +333,13 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
                     if (u0 + h4 + i < v) dd[i] = (uint32_t)row[u0 + h4 + i];
             }
             // per candidate: exists / accepted outright (δ <= 0, R5) / needs the threshold test
-            unsigned need = 0;
+            unsigned need = 0, am = 0;
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                const int o = rb[i] + v;
+                const int o = rb[4 * g + i] + v;
                 const int d = (int)dd[i];
-                const bool ex = h4 + i < R && v >= rf[i] && vin && o < Wl;
-                acc_mask |= (unsigned)(ex && d <= 0) << i;
+                const bool ex = h4 + i < R && v >= rf[4 * g + i] && vin && o < Wl;
+                am |= (unsigned)(ex && d <= 0) << i;
                 need |= (unsigned)(ex && d > 0 && d <= rejI) << i;   // above rejI: certain reject
             }
 #if defined(TC_EXP) && (TC_EXP & 2)
@@ -345,7 +350,7 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     if ((need >> i) & 1u) {
-                        const int o = rb[i] + v;
+                        const int o = rb[4 * g + i] + v;
                         const int d = (int)dd[i];
                         float th, m;
                         if (o < pnk) { const float2 q = thm[o]; th = q.x; m = q.y; }
@@ -355,25 +360,26 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
                         if (!ac && !(df > th + m)) {  // inside the margin: exact double test (R16)
                             const int x = tc_exact(d, k + (uint64_t)o, sch, seed);
                             ac = x & 1;
-                            near_mask |= (unsigned)((x >> 1) & 1) << i;
+                            near_mask |= (unsigned)((x >> 1) & 1) << (4 * g + i);
                         }
-                        acc_mask |= (unsigned)ac << i;
+                        am |= (unsigned)ac << i;
                     }
                 }
             }
-            // first accepted candidate of this thread (offsets grow with i)
-            int best_o = INT_MAX, best_d = 0, best_rs = 0;
+            acc_mask |= am << (4 * g);
+            // first accepted candidate of this thread (offsets grow with the row)
 #pragma unroll
             for (int i = 3; i >= 0; --i) {
-                const bool ac = (acc_mask >> i) & 1u;
-                best_o = ac ? rb[i] + v : best_o;
-                best_d = ac ? (int)dd[i] : best_d;
-                best_rs = ac ? ((u0 + h4 + i) | (v << 8) | (pu[i] << 16) | (px << 24)) : best_rs;
+                const bool ac = (am >> i) & 1u;
+                const bool better = ac && rb[4 * g + i] + v < best_o;
+                best_o = better ? rb[4 * g + i] + v : best_o;
+                best_d = better ? (int)dd[i] : best_d;
+                best_rs = better ? ((u0 + h4 + i) | (v << 8) | (pu[i] << 16) | (px << 24)) : best_rs;
             }
+        }
+        {
             const int wmin = __reduce_min_sync(0xffffffffu, best_o);
             if (best_o == wmin && (wmin != INT_MAX || lane == 0)) sl[warp] = make_int4(best_o, best_d, best_rs, 0);
-        } else if (lane == 0) {
-            sl[warp] = make_int4(INT_MAX, 0, 0, 0);
         }
         TCT_ACC(10, pt0, acc_mask);
         tc::fence_before_sync();
@@ -387,7 +393,7 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
         const int consumed = (j == INT_MAX) ? Wl : j + 1;
         if (near_mask) {                         // R16: log near ties of consumed iterations
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
+            for (int i = 0; i < 8; ++i) {
                 const int o = rb[i] + v;
                 if (((near_mask >> i) & 1u) && o < consumed) {
                     const unsigned int e = atomicAdd(sink.count, 1u);
