@@ -311,8 +311,8 @@ int orc_sa_run(orc_state* st, uint64_t k0, uint64_t iters, int kind, double t0, 
                 st->best_cost = st->cost;
                 memcpy(st->best_p, st->p, sizeof(int32_t) * (size_t)n);
             }
-            st->digest = mix64(st->digest ^ k);
-            st->digest = mix64(st->digest ^ (((uint64_t)(uint32_t)r << 32) | (uint32_t)s));
+            /* R18: wrapping sum of one hash per accepted (k, r, s) */
+            st->digest += mix64(mix64(k) ^ (((uint64_t)(uint32_t)r << 32) | (uint32_t)s));
             if (check_every > 0 && (int64_t)(st->accepted % (uint64_t)check_every) == 0) {
                 if (check_state(st) != 0) { status = -1; st->iterations += it + 1; goto done; }
             }

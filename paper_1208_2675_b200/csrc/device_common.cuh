@@ -106,7 +106,9 @@ __device__ __forceinline__ void tri_pair(int n, int q, int* r, int* s) {
     *s = q - tri_base(n, rr) + rr + 1;
 }
 
-// ---- trajectory digest (R18): splitmix64 finaliser, two mixes per accept.
+// ---- trajectory digest (R18): wrapping sum over the accepted (k, r, s) of
+// mix(mix(k) ^ (r << 32 | s)), mix = splitmix64 finaliser.  The sum does not depend
+// on the order in which accepts are added, so batches of accepts hash in parallel.
 __host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
     x += 0x9E3779B97F4A7C15ull;
     x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -114,8 +116,7 @@ __host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
     return x ^ (x >> 31);
 }
 __host__ __device__ __forceinline__ uint64_t digest_step(uint64_t d, uint64_t k, int r, int s) {
-    d = mix64(d ^ k);
-    return mix64(d ^ (((uint64_t)(uint32_t)r << 32) | (uint32_t)s));
+    return d + mix64(mix64(k) ^ (((uint64_t)(uint32_t)r << 32) | (uint32_t)s));
 }
 constexpr uint64_t kDigestSeed = 0x9E3779B97F4A7C15ull;
 
