@@ -186,14 +186,23 @@ typedef enum {
                                     rank update on the tensor cores when the instance allows it
                                     (4 <= n <= 128, all entries <= 127), else the shared-memory
                                     kernel; 0 = always the shared-memory kernel */
-    QAP_OPT_SCRATCH_PHASE = 6    /* tensor-memory engine only: 1 (default) = run the high-acceptance
+    QAP_OPT_SCRATCH_PHASE = 6,   /* tensor-memory engine only: 1 (default) = run the high-acceptance
                                     start of each qap_sa_run without Δ (δ from G = A B'^T, SURVEY
                                     f2) until no swap is accepted for 4096 iterations, then rebuild
                                     Δ and continue with Δ; 0 = Δ throughout.  Same trajectory. */
+    QAP_OPT_RELABEL = 7          /* instances with 8-bit A and 16-bit B, 4 <= n <= 256 (config 4):
+                                    1 (default) = relabel engine: swaps of twin locations (equal
+                                    rows of A off the pair, R21) are exact O(1) index
+                                    relabels, other swaps the ordinary update;
+                                    2 = the same engine with the relabels off; 0 = the
+                                    shared-memory kernel.  Same trajectory in every case. */
 } qap_option;
 qap_status qap_set_option(qap_ctx* ctx, int32_t key, int64_t value);
 /* 1 if the next qap_sa_run uses the tensor-memory engine (QAP_OPT_TENSOR_CORE), else 0. */
 int32_t qap_uses_tensor_core(const qap_ctx* ctx);
+/* The engine the next qap_sa_run uses (QAP_ENGINE_*), -1 if ctx is NULL. */
+enum { QAP_ENGINE_SHARED_MEMORY = 0, QAP_ENGINE_TENSOR_MEMORY = 1, QAP_ENGINE_RELABEL = 2 };
+int32_t qap_engine(const qap_ctx* ctx);
 
 /* Device time in milliseconds of the last qap_sa_run kernel (CUDA events
  * on the context stream), and the number of kernels the last call launched. */

@@ -34,7 +34,7 @@ struct ChainResult {              // mirrors qap_chain_result
 struct GroupLayout {
     int bp, d, dab, dg, p, bestp, slots, flags, bytes;
 };
-__host__ __device__ inline int align16(int x) { return (x + 15) & ~15; }
+__host__ __device__ constexpr int align16(int x) { return (x + 15) & ~15; }
 // dab_bytes: 4 when A and B are both 8-bit (packed int16 pair), else 8
 // nqt: number of Δ quads (quad layout, chain.cuh)
 __host__ __device__ inline GroupLayout group_layout(int n, int ld, int nqt, int tb_bytes, int nw,

@@ -7,6 +7,7 @@
 // fallback: without an sm_100 device the calls fail with QAP_E_CUDA.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -18,6 +19,7 @@
 #include "kernels.cuh"
 #include "tc_chain.cuh"
 #include "scratch_chain.cuh"
+#include "relabel_chain.cuh"
 
 using namespace qapsa;
 
@@ -57,6 +59,12 @@ struct qap_ctx {
     unsigned long long last_scratch[2] = {0, 0};   // iteration reached, accepted swaps
     float last_ms = 0.f;
     int last_launches = 0;
+    // relabel engine (relabel_chain.cuh): twin classes of A, second Δ buffer for the write-back
+    int use_relabel = 1;                // QAP_OPT_RELABEL
+    int ncls = 0;
+    uint8_t* dcls = nullptr;            // n
+    uint16_t* dpt = nullptr;            // ncls x (n+1)
+    int32_t* dD2 = nullptr;             // quad layout, same size as dD
 };
 
 static thread_local std::string g_static_err;
@@ -137,6 +145,52 @@ static void quad_tables(int n, std::vector<int32_t>* rowaddr, std::vector<uint16
     }
 }
 
+// Twin classes of A (R21): x ~ y iff A_xz == A_yz for every z != x, y.  A class is kept only if
+// all its members are pairwise twins; the RLB_MAXCLS largest classes with >= 2 members get
+// indices, every other location 0xFF (its swaps take the ordinary update, which is exact for
+// any pair).  pt[c][x] = largest member of class c below x, 0xFFFF if none.
+static void twin_classes(int n, const int32_t* A, std::vector<uint8_t>* cls, std::vector<uint16_t>* pt,
+                         int* ncls) {
+    auto twin = [&](int x, int y) {
+        for (int z = 0; z < n; ++z)
+            if (z != x && z != y && A[(size_t)x * n + z] != A[(size_t)y * n + z]) return false;
+        return true;
+    };
+    std::vector<std::vector<int>> classes;
+    for (int x = 0; x < n; ++x) {
+        bool placed = false;
+        for (auto& cl : classes) {
+            if (!twin(cl[0], x)) continue;
+            bool all = true;
+            for (int y : cl) all = all && twin(y, x);
+            if (all) { cl.push_back(x); placed = true; break; }
+        }
+        if (!placed) classes.push_back({x});
+    }
+    std::vector<int> order;
+    for (int i = 0; i < (int)classes.size(); ++i)
+        if (classes[i].size() >= 2) order.push_back(i);
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int a, int b) { return classes[a].size() > classes[b].size(); });
+    if ((int)order.size() > RLB_MAXCLS) order.resize(RLB_MAXCLS);
+    cls->assign(n, 0xFF);
+    *ncls = (int)order.size();
+    pt->assign((size_t)(*ncls) * (n + 1), 0xFFFF);
+    for (int c = 0; c < *ncls; ++c) {
+        for (int x : classes[order[c]]) (*cls)[x] = (uint8_t)c;
+        int last = 0xFFFF;
+        for (int x = 0; x <= n; ++x) {
+            (*pt)[(size_t)c * (n + 1) + x] = (uint16_t)last;
+            if (x < n && (*cls)[x] == c) last = x;
+        }
+    }
+}
+
+static bool use_relabel_engine(const qap_ctx* c) {
+    return c->use_relabel && c->ta == 1 && c->tb == 2 && c->n >= 4 && c->n <= RLB_MAXN &&
+           rlb_layout(c->n).bytes <= c->smem_optin;
+}
+
 static qap_status validate_schedule(qap_ctx* c, const qap_schedule* s, uint64_t k0, uint64_t iters,
                                     Sched* out) {
     if (!s) return fail(c, QAP_E_INVALID_ARG, "schedule is NULL");
@@ -189,7 +243,7 @@ void qap_destroy(qap_ctx* c) {
     void* ptrs[] = {c->dA, c->dB, c->dp0, c->dp, c->dbest, c->dD, c->dperm, c->dDlin, c->drowaddr,
                     c->dqdesc, c->dst, c->dnear_count,
                     c->dnear_k, c->dnear_dec, c->dscratch, c->ens_p0, c->ens_res, c->ens_best,
-                    c->ens_counter, c->dkout};
+                    c->ens_counter, c->dkout, c->dcls, c->dpt, c->dD2};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->ev0) cudaEventDestroy(c->ev0);
@@ -284,6 +338,12 @@ qap_status qap_create(int32_t n, const int32_t* A, const int32_t* B, const int32
     alloc((void**)&c->dnear_dec, QAP_NEAR_LOG_CAP);
     alloc((void**)&c->dscratch, 8 * sizeof(long long));
     alloc((void**)&c->dkout, 2 * sizeof(unsigned long long));
+    alloc((void**)&c->dD2, (size_t)c->nqt * 16 + 16);
+    std::vector<uint8_t> hcls;
+    std::vector<uint16_t> hpt;
+    twin_classes(n, A, &hcls, &hpt, &c->ncls);
+    alloc((void**)&c->dcls, (size_t)n + 16);
+    alloc((void**)&c->dpt, hpt.size() * 2 + 16);
     if (st != QAP_OK) {
         qap_destroy(c);
         return st;
@@ -298,6 +358,9 @@ qap_status qap_create(int32_t n, const int32_t* A, const int32_t* B, const int32
     if (e == cudaSuccess) e = cudaMemcpyAsync(c->dp0, p0, n * 4, cudaMemcpyHostToDevice, c->stream);
     if (e == cudaSuccess) e = cudaMemcpyAsync(c->drowaddr, hrow.data(), n * 4, cudaMemcpyHostToDevice, c->stream);
     if (e == cudaSuccess) e = cudaMemcpyAsync(c->dqdesc, hq.data(), hq.size() * 2, cudaMemcpyHostToDevice, c->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(c->dcls, hcls.data(), n, cudaMemcpyHostToDevice, c->stream);
+    if (e == cudaSuccess && !hpt.empty()) e = cudaMemcpyAsync(c->dpt, hpt.data(), hpt.size() * 2, cudaMemcpyHostToDevice, c->stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(c->dD2, 0, (size_t)c->nqt * 16 + 16, c->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);   // host tables go out of scope
     if (e != cudaSuccess) {
         std::string m = cudaGetErrorString(e);
@@ -434,10 +497,13 @@ qap_status qap_sa_run(qap_ctx* c, uint64_t k0, uint64_t iters, const qap_schedul
     CU(cudaMemcpyAsync(&near_before, c->dnear_count, sizeof near_before, cudaMemcpyDeviceToHost, c->stream));
 
     const bool tc = use_tc_engine(c);
+    const bool rlb = !tc && use_relabel_engine(c);
     const bool explicit_threads = c->threads != 0;
     const int threads = tc ? TCK_NT : effective_threads(c, explicit_threads ? c->threads : auto_threads(c));
     bool ds = !c->force_global && chain_smem_bytes(c, threads, true) <= c->smem_optin;
-    const int smem = tc ? tc_layout(c->ld).bytes : chain_smem_bytes(c, threads, ds);
+    const int smem = tc ? tc_layout(c->ld).bytes
+                        : rlb ? rlb_layout(c->n).bytes
+                              : chain_smem_bytes(c, threads, ds);
     if (smem > c->smem_optin) return fail(c, QAP_E_UNSUPPORTED, "chain state does not fit on chip");
 
     ChainArgs a;
@@ -473,6 +539,18 @@ qap_status qap_sa_run(qap_ctx* c, uint64_t k0, uint64_t iters, const qap_schedul
         }
         kern<<<1, TCK_NT, smem, c->stream>>>(a);
         CU(cudaGetLastError());
+    } else if (rlb) {
+        RelabelArgs ra;
+        ra.c = a;
+        ra.cls = c->dcls;
+        ra.pt = c->dpt;
+        ra.ncls = c->use_relabel == 2 ? 0 : c->ncls;
+        ra.d_out = c->dD2;
+        auto kern = c->n == 256 ? k_sa_relabel<256> : k_sa_relabel<0>;
+        CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        kern<<<1, RLB_NT, smem, c->stream>>>(ra);
+        CU(cudaGetLastError());
+        std::swap(c->dD, c->dD2);              // Δ in location space is in the second buffer
     } else {
         CU(launch_chain(c, a, threads, explicit_threads, ds, smem));
     }
@@ -711,6 +789,10 @@ qap_status qap_set_option(qap_ctx* c, int32_t key, int64_t value) {
         case QAP_OPT_SCRATCH_PHASE:
             c->use_scratch = value ? 1 : 0;
             return QAP_OK;
+        case QAP_OPT_RELABEL:
+            if (value < 0 || value > 2) return fail(c, QAP_E_INVALID_ARG, "relabel must be 0, 1 or 2");
+            c->use_relabel = (int)value;
+            return QAP_OK;
         case QAP_OPT_ENSEMBLE_GROUP:
             if (value != 64 && value != 128 && value != 256) return fail(c, QAP_E_INVALID_ARG, "group must be 64, 128 or 256");
             c->ens_group = (int)value;
@@ -720,6 +802,13 @@ qap_status qap_set_option(qap_ctx* c, int32_t key, int64_t value) {
 }
 
 int32_t qap_uses_tensor_core(const qap_ctx* c) { return (c && use_tc_engine(c)) ? 1 : 0; }
+
+int32_t qap_engine(const qap_ctx* c) {
+    if (!c) return -1;
+    if (use_tc_engine(c)) return QAP_ENGINE_TENSOR_MEMORY;
+    if (use_relabel_engine(c)) return QAP_ENGINE_RELABEL;
+    return QAP_ENGINE_SHARED_MEMORY;
+}
 
 qap_status qap_last_scratch_time(qap_ctx* c, float* ms, uint64_t* k_reached, uint64_t* accepted) {
     CHECK_CTX(c);

@@ -24,12 +24,14 @@ QAP_COOL_GEOMETRIC, QAP_COOL_LUNDY_MEES = 0, 1
 QAP_OPT_WINDOW_MAX, QAP_OPT_THREADS, QAP_OPT_FORCE_GLOBAL_DELTA, QAP_OPT_ENSEMBLE_GROUP = 1, 2, 3, 4
 QAP_OPT_TENSOR_CORE = 5
 QAP_OPT_SCRATCH_PHASE = 6
+QAP_OPT_RELABEL = 7
+QAP_ENGINE_SHARED_MEMORY, QAP_ENGINE_TENSOR_MEMORY, QAP_ENGINE_RELABEL = 0, 1, 2
 QAP_NEAR_LOG_CAP = 1024
 
 # Every symbol include/qapsa.h declares (checked by tests/test_abi.py).
 EXPORTS = ("qap_create", "qap_destroy", "qap_reset", "qap_delta_init", "qap_sa_run", "qap_cost",
            "qap_get_state", "qap_get_near_ties", "qap_schedule_bounds", "qap_ensemble_run",
-           "qap_set_option", "qap_uses_tensor_core", "qap_last_kernel_time", "qap_last_scratch_time",
+           "qap_set_option", "qap_uses_tensor_core", "qap_engine", "qap_last_kernel_time", "qap_last_scratch_time",
            "qap_status_str",
            "qap_last_error", "qap_version")
 
@@ -99,9 +101,11 @@ def lib(build_if_missing: bool = True):
     L.qap_version.restype = C.c_int32
     L.qap_uses_tensor_core.argtypes = [vp]
     L.qap_uses_tensor_core.restype = C.c_int32
+    L.qap_engine.argtypes = [vp]
+    L.qap_engine.restype = C.c_int32
     for name in EXPORTS:
         if name not in ("qap_destroy", "qap_status_str", "qap_last_error", "qap_version",
-                        "qap_uses_tensor_core"):
+                        "qap_uses_tensor_core", "qap_engine"):
             getattr(L, name).restype = C.c_int
     _lib = L
     return L
@@ -230,6 +234,11 @@ def qap_uses_tensor_core(ctx) -> bool:
     return bool(lib().qap_uses_tensor_core(ctx))
 
 
+def qap_engine(ctx) -> int:
+    """QAP_ENGINE_* of the next qap_sa_run."""
+    return int(lib().qap_engine(ctx))
+
+
 def qap_last_scratch_time(ctx):
     """(ms, iteration reached, swaps accepted) of the last run's scratch phase."""
     ms, kr, acc = C.c_float(), C.c_uint64(), C.c_uint64()
@@ -309,6 +318,9 @@ class Solver:
 
     def uses_tensor_core(self) -> bool:
         return qap_uses_tensor_core(self.ctx)
+
+    def engine(self) -> int:
+        return qap_engine(self.ctx)
 
     def ensemble(self, chain_begin, p0s, iters, schedule, seed, per_chain=False):
         return qap_ensemble_run(self.ctx, chain_begin, p0s, iters, schedule, seed, per_chain)

@@ -18,7 +18,7 @@ from __future__ import annotations
 import numpy as np
 
 __all__ = [
-    "taixxa", "grey_density", "start_perm", "start_perms", "config",
+    "taixxa", "grey_density", "block_classes", "start_perm", "start_perms", "config",
     "CONFIGS",
 ]
 
@@ -64,6 +64,34 @@ def grey_density(n: int = 256, m: int = 92, side: int = 16):
     d = dx + dy
     B = (255 * (side - d) ** 2).astype(np.int32)
     np.fill_diagonal(B, 0)
+    return np.ascontiguousarray(A), np.ascontiguousarray(B)
+
+
+def block_classes(n: int, sizes, seed: int, hi_a: int = 99, hi_b: int = 60000):
+    """Instance whose flow matrix A has twin locations (R21), like config 4.
+
+    Locations are labelled: the first sizes[0] locations class 0, the next sizes[1] class 1, ...,
+    every remaining location its own label; the labels are then shuffled over the locations.
+    A_xy = V[label x][label y] (x != y) for a random symmetric V uniform on 0..hi_a, so all
+    members of a class have equal rows off the pair.  B is symmetric, zero diagonal, uniform
+    on 0..hi_b (16-bit when hi_b > 255).  numpy PCG64(seed).
+    """
+    rng = np.random.Generator(np.random.PCG64(seed))
+    labels = []
+    for c, m in enumerate(sizes):
+        labels += [c] * m
+    nl = len(sizes)
+    labels += list(range(nl, nl + n - len(labels)))
+    labels = rng.permutation(np.array(labels, dtype=np.int64))
+    L = int(labels.max()) + 1
+    V = rng.integers(0, hi_a + 1, size=(L, L), dtype=np.int64)
+    V = np.triu(V) + np.triu(V, 1).T
+    A = V[labels[:, None], labels[None, :]].astype(np.int32)
+    np.fill_diagonal(A, 0)
+    iu = np.triu_indices(n, 1)
+    B = np.zeros((n, n), dtype=np.int32)
+    B[iu] = rng.integers(0, hi_b + 1, size=iu[0].size, dtype=np.int64).astype(np.int32)
+    B = B + B.T
     return np.ascontiguousarray(A), np.ascontiguousarray(B)
 
 

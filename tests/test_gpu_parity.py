@@ -8,7 +8,7 @@ import pytest
 
 import oracle as O
 from paper_1208_2675_b200 import qapsa as Q
-from qap_inputs import SA_SEED, config, grey_density, start_perm, start_perms, taixxa
+from qap_inputs import SA_SEED, block_classes, config, grey_density, start_perm, start_perms, taixxa
 
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
@@ -22,6 +22,11 @@ SCR = Q.QAP_OPT_SCRATCH_PHASE
 # eligible), tensor memory with Δ throughout, shared memory
 ENGINES = [pytest.param([(TC, 1), (SCR, 1)], id="tmem"), pytest.param([(TC, 1), (SCR, 0)], id="tmem_delta"),
            pytest.param([(TC, 0)], id="smem")]
+RLB = Q.QAP_OPT_RELABEL
+# instances with 8-bit A and 16-bit B (config 4): the relabel engine, the same engine with the
+# twin relabels off, the shared-memory engine
+RELABEL_ENGINES = [pytest.param([(RLB, 1)], id="relabel"), pytest.param([(RLB, 2)], id="wide"),
+                   pytest.param([(RLB, 0)], id="smem")]
 
 
 def _sched(s: O.Schedule):
@@ -258,14 +263,62 @@ def test_schedule_errors():
             assert e.value.status == 5
 
 
-def test_grey_density_uint16_prefix():
+@pytest.mark.parametrize("engine", RELABEL_ENGINES)
+def test_grey_density_uint16_prefix(engine):
     """Config-4-shaped instance (uint16 B, δ≡0 plateau): first 3e5 iterations of
     its 1e9-iteration schedule, Δ spilled to global memory."""
     A, B = grey_density(256)
     p0 = start_perm(256, SA_SEED, 0)
     sch = O.geometric_schedule_for(A, B, p0, 10**9)
-    g, acc = _compare_run(A, B, p0, 300000, sch, mode=O.MODE_SCRATCH)
+    g, acc = _compare_run(A, B, p0, 300000, sch, mode=O.MODE_SCRATCH, opts=engine)
     assert acc > 100000
+
+
+def test_relabel_engine_selection():
+    for (A, B), want in [(grey_density(256), Q.QAP_ENGINE_RELABEL),
+                         (block_classes(40, [6, 3], 1), Q.QAP_ENGINE_RELABEL),
+                         (block_classes(40, [6, 3], 1, hi_b=99), Q.QAP_ENGINE_TENSOR_MEMORY),
+                         (taixxa(150, 1), Q.QAP_ENGINE_SHARED_MEMORY)]:
+        n = A.shape[0]
+        with Q.Solver(A, B, start_perm(n, 1, 0)) as s:
+            assert s.engine() == want
+            s.set_option(RLB, 0)
+            if want == Q.QAP_ENGINE_RELABEL:
+                assert s.engine() == Q.QAP_ENGINE_SHARED_MEMORY
+
+
+@pytest.mark.parametrize("n,sizes,seed,iters", [(4, [2], 1, 3000), (9, [3, 2], 2, 20000),
+                                                (33, [8, 5, 3], 3, 50000),
+                                                (64, [20, 10, 6, 3], 4, 100000),
+                                                (130, [40, 30, 2], 5, 60000),
+                                                (256, [92, 100, 3], 6, 60000)])
+@pytest.mark.parametrize("engine", RELABEL_ENGINES[:2])
+def test_relabel_engine_twin_classes(n, sizes, seed, iters, engine):
+    """Instances with twin classes (R21) and 16-bit B: Δ, p, best_p, C, digest and every
+    counter bit-exact against the oracle in DELTA mode, relabels on and off."""
+    A, B = block_classes(n, sizes, seed, hi_b=20000)     # 4 n maxA maxB < 2^31 (R13)
+    p0 = start_perm(n, seed, 0)
+    sch = O.geometric_schedule_for(A, B, p0, iters)
+    _compare_run(A, B, p0, iters, sch, opts=engine)
+
+
+@pytest.mark.parametrize("engine", RELABEL_ENGINES[:2])
+def test_relabel_engine_no_twins_and_resume(engine):
+    """A 16-bit instance without twins (the wide engine's ordinary path), and a twin instance
+    split into uneven calls (σ is folded back into p and Δ at every exit)."""
+    A, _ = taixxa(77, 77)
+    _, B = taixxa(77, 78, hi=3000)
+    p0 = start_perm(77, 7, 0)
+    with Q.Solver(A, B, p0) as s:
+        for k, v in engine:
+            s.set_option(k, v)
+        assert s.engine() == Q.QAP_ENGINE_RELABEL
+    _compare_run(A, B, p0, 40000, O.geometric_schedule_for(A, B, p0, 40000), opts=engine)
+    A, B = block_classes(101, [30, 20, 10], 8, hi_b=20000)
+    p0 = start_perm(101, 8, 0)
+    I = 50000
+    _compare_run(A, B, p0, I, O.geometric_schedule_for(A, B, p0, I), opts=engine,
+                 k_splits=[0, 1, 77, 5000, 5001, 23456, I])
 
 
 # ---------------- a8: ensemble ----------------

@@ -278,3 +278,34 @@ def test_swap_then_delta_is_negated():
     O.apply_swap(p, Bp, 3, 8)
     O.update_delta(A, pre, Bp, 3, 8, D)
     assert D[O.index(11, 3, 8)] == -d
+
+
+def test_twin_swaps_are_cost_neutral():
+    """R21 (relabel engine): if rows x and y of A agree off the pair (twins), exchanging the
+    facilities of x and y leaves Eq.(1) unchanged for EVERY permutation, so δ(x,y) = 0 in every
+    state and the oracle's Δ holds 0 there.  Checked by direct Eq.(1) sums (numpy) on random
+    permutations of an instance with twin classes, and on config 4's grey-density A."""
+    from qap_inputs import block_classes, grey_density
+    for A, B in (block_classes(24, [5, 4, 2], 7), grey_density(16, 6, 4)):
+        n = A.shape[0]
+        twins = [(x, y) for x in range(n) for y in range(x + 1, n)
+                 if all(A[x, z] == A[y, z] for z in range(n) if z not in (x, y))]
+        assert len(twins) >= 10
+        rng = np.random.default_rng(3)
+
+        def eq1(p):
+            return int((A.astype(np.int64) * B[np.ix_(p, p)]).sum())
+
+        nonzero = 0
+        for _ in range(20):
+            p = rng.permutation(n)
+            c0 = eq1(p)
+            for x, y in twins:
+                q = p.copy()
+                q[x], q[y] = q[y], q[x]
+                assert eq1(q) == c0
+            D = O.delta_init(A, O.bprime(B, p.astype(np.int32)))
+            for x, y in twins:
+                assert D[x * n - x * (x + 1) // 2 + y - x - 1] == 0
+            nonzero += int(np.count_nonzero(D))
+        assert nonzero > 0                      # the other swaps do change the cost
