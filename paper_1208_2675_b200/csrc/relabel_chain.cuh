@@ -19,16 +19,20 @@
 // thread adds its accept to a private count and digest (R18 is a sum).
 //
 // Per cross accept (slots a < b), 1024 threads:
-//   stage   dA_x = A_ax - A_bx, dB_x = B~_ax - B~_bx; Z_a = A_a.B~_b, Z_b = A_b.B~_a (warps 8, 9)
-//   touch   threads 0..511, 2 per v: X_a = B~_v.A_a, X_b, Y_a = A_v.B~_a, Y_b over half of the
-//           row each, shuffle-reduced; δ''(a,v), δ''(b,v) (R10b) and D~_v written
-//   quads   threads 512..1023, concurrently: Δ~ += 2(dA_u - dA_v)(dB_u - dB_v) for every pair
-//           off rows / columns a, b (R10); Δ~ in global memory / L2 (quad layout)
+//   stage   dA_x = A_ax - A_bx, dB_x = B~_ax - B~_bx; Z_a = A_a.B~_b, Z_b = A_b.B~_a (warps 8, 9);
+//           the 8 columns of the MMA's B operand from rows a, b (threads 0..127)
+//   touch   the four dot products of every v, X_a = B~_v.A_a, X_b, Y_a = A_v.B~_a, Y_b, are two
+//           GEMVs: ONE tensor-core product [Bh | Bl | A] (256 x 768, u8) x W (768 x 8, u8), with
+//           B~ = 256 Bh + Bl split into bytes and W's columns (A_a;0;0), (A_b;0;0), (0;A_a;0),
+//           (0;A_b;0), (0;0;Bl_a), (0;0;Bh_a), (0;0;Bl_b), (0;0;Bh_b): 2 x 24 tcgen05.mma
+//           (kind::i8, M = 128, N = 8, K = 32, s32 in TMEM, exact).  Warps 0..7 read the
+//           result (one TMEM lane per v) and write δ''(a,v), δ''(b,v) (R10b) and D~_v
+//   quads   all threads while the MMAs run: Δ~ += 2(dA_u - dA_v)(dB_u - dB_v) for every pair
+//           off rows a, b (R10), one 16-byte quad at a time; Δ~ in global memory / L2
 //   next window: B~ rows / columns a, b exchanged, best_p = q∘σ if the cost improved
 //
-// Shared memory (N = 256): A 256 x 272 B (odd multiple of 16 B per row) and B~ 256 x 264 u16
-// (528 B = 33 x 16 B per row): the 8 rows one warp reads at the same column offset fall on
-// distinct 16-byte bank groups.
+// Shared memory (N = 256): the MMA's A operand [Bh | Bl | A] in the K-major canonical layout
+// (tc_common.cuh), 192 KB, is the only copy of A and B~.
 //
 // Citation keys: P:n = PAPER.md line n, R# = DESIGN.md readings.
 #pragma once
@@ -36,28 +40,29 @@
 #include <cstdint>
 
 #include "kernels.cuh"
+#include "tc_common.cuh"
 
 namespace qapsa {
 
 constexpr int RLB_NT = 1024;
 constexpr int RLB_MAXN = 256;
 constexpr int RLB_MAXCLS = 4;   // twin classes (>= 2 members) the relabel path handles
-constexpr int RLB_TOUCH = 512;  // threads [0, 512): touching entries (2 per v); the rest: quads
+constexpr int RLB_EPI = 256;    // threads [0, 256): MMA issue and touching epilogue (after their quads)
 constexpr int RLB_QB = 4;       // quad loads in flight per thread
-
-// row strides in shared memory: A an odd multiple of 16 elements (bytes), B~ 8 x odd elements
-__host__ __device__ constexpr int rlb_lda(int n) { return row_stride(n, true); }
-__host__ __device__ constexpr int rlb_ldb(int n) { return 16 * ((n + 15) / 16) + 8; }
+constexpr int RLB_K = 768;      // K of the touching product: Bh | Bl | A
+constexpr int RLB_SBO = RLB_K / 16 * 128;        // 8-row group stride of the canonical layout
+constexpr int RLB_BL = 256, RLB_AOFF = 512;      // K offsets of the Bl and A parts
 
 struct RlbLayout {
-    int a, b, rowaddr, qdesc, pt, cls, sig, q, bestp, dg, stg, slots, twm, zz, flags, red, bytes;
+    int op1, op2, rowaddr, qdesc, pt, cls, sig, q, bestp, dg, stg, slots, twm, zz, flags, red, bar,
+        bytes;
 };
 __host__ __device__ constexpr RlbLayout rlb_layout(int n) {
     RlbLayout L{};
     const int n4 = (n + 3) & ~3;
     int o = 0;
-    L.a = o;       o = align16(o + n * rlb_lda(n));
-    L.b = o;       o = align16(o + n * rlb_ldb(n) * 2);
+    L.op1 = o;     o += RLB_MAXN / 8 * RLB_SBO;          // 256 rows x 768 B, canonical K-major
+    L.op2 = o;     o += RLB_SBO;                        // 8 rows x 768 B
     L.rowaddr = o; o = align16(o + n * 4);
     L.qdesc = o;   o = align16(o + quad_count(n) * 2);
     L.pt = o;      o = align16(o + RLB_MAXCLS * (n + 1) * 2);
@@ -66,12 +71,13 @@ __host__ __device__ constexpr RlbLayout rlb_layout(int n) {
     L.q = o;       o = align16(o + n * 2);
     L.bestp = o;   o = align16(o + n * 2);
     L.dg = o;      o = align16(o + n * 4);
-    L.stg = o;     o = align16(o + n4 * 8);
+    L.stg = o;     o = align16(o + n4 * 4);
     L.slots = o;   o = align16(o + 2 * 32 * 16);
     L.twm = o;     o = align16(o + 2 * 32 * 4);
     L.zz = o;      o = align16(o + 4 * 4);
     L.flags = o;   o = align16(o + 4 * 4);
     L.red = o;     o = align16(o + 2 * 8);
+    L.bar = o;     o = align16(o + 16);                 // mbarrier + TMEM base address
     L.bytes = o;
     return L;
 }
@@ -84,28 +90,11 @@ struct RelabelArgs {
     int32_t* d_out;            // Δ in location space at exit (quad layout)
 };
 
-// X_a += B~_v.A_a, X_b += B~_v.A_b, Y_a += A_v.B~_a, Y_b += A_v.B~_b over blocks b0, b0+step, ..
-__device__ __forceinline__ void rlb_dots(const uint8_t* Av, const uint16_t* Bv, const uint8_t* Aa,
-                                         const uint8_t* Ab, const uint16_t* Ba, const uint16_t* Bb,
-                                         int b0, int step, int nb, int& xa, int& xb, int& ya, int& yb) {
-    const uint4* av = reinterpret_cast<const uint4*>(Av);
-    const uint4* bv = reinterpret_cast<const uint4*>(Bv);
-    const uint4* aa = reinterpret_cast<const uint4*>(Aa);
-    const uint4* ab = reinterpret_cast<const uint4*>(Ab);
-    const uint4* ba = reinterpret_cast<const uint4*>(Ba);
-    const uint4* bb = reinterpret_cast<const uint4*>(Bb);
-    uint32_t Xa = 0, Xb = 0, Ya = 0, Yb = 0;
-#pragma unroll 2
-    for (int b = b0; b < nb; b += step) {
-        const uint4 a = av[b], v0 = bv[2 * b], v1 = bv[2 * b + 1];
-        const uint4 a8 = aa[b], b8 = ab[b];
-        const uint4 A0 = ba[2 * b], A1 = ba[2 * b + 1], B0 = bb[2 * b], B1 = bb[2 * b + 1];
-        Xa = dp16w(a8, v0, v1, Xa);
-        Xb = dp16w(b8, v0, v1, Xb);
-        Ya = dp16w(a, A0, A1, Ya);
-        Yb = dp16w(a, B0, B1, Yb);
-    }
-    xa += (int)Xa; xb += (int)Xb; ya += (int)Ya; yb += (int)Yb;
+// element accessors of the canonical operand (row x, K offset k)
+__device__ __forceinline__ int rlb_off(int x, int k) { return tc::kmaj_off(x, k, RLB_SBO); }
+__device__ __forceinline__ int rlb_A(const uint8_t* op1, int x, int k) { return op1[rlb_off(x, RLB_AOFF + k)]; }
+__device__ __forceinline__ int rlb_B(const uint8_t* op1, int x, int k) {
+    return ((int)op1[rlb_off(x, k)] << 8) | (int)op1[rlb_off(x, RLB_BL + k)];
 }
 
 template <int NFIX>
@@ -114,14 +103,14 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
     const ChainArgs& a = ra.c;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int n = NFIX ? NFIX : a.n;
-    const int lda = rlb_lda(n), ldb = rlb_ldb(n), ldg = a.ld;
-    const int nb = (n + 15) >> 4;
+    const int ldg = a.ld;
     const int M = n * (n - 1) / 2;
     const int nqt = NFIX ? quad_count(NFIX) : a.nqt;
+    const int nq4 = (n + 3) >> 2;                        // 16-byte chunks per row
     const int ncls = ra.ncls;
     const RlbLayout L = rlb_layout(n);
-    uint8_t* As = smem + L.a;
-    uint16_t* Bt = reinterpret_cast<uint16_t*>(smem + L.b);
+    uint8_t* op1 = smem + L.op1;
+    uint8_t* op2 = smem + L.op2;
     int32_t* rowaddr = reinterpret_cast<int32_t*>(smem + L.rowaddr);
     uint16_t* qdesc = reinterpret_cast<uint16_t*>(smem + L.qdesc);
     uint16_t* pt = reinterpret_cast<uint16_t*>(smem + L.pt);
@@ -130,21 +119,19 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
     uint16_t* q = reinterpret_cast<uint16_t*>(smem + L.q);
     uint16_t* bestp = reinterpret_cast<uint16_t*>(smem + L.bestp);
     int32_t* Dg = reinterpret_cast<int32_t*>(smem + L.dg);
-    int2* stg = reinterpret_cast<int2*>(smem + L.stg);
+    int32_t* stg = reinterpret_cast<int32_t*>(smem + L.stg);   // 2 (1024 dB_x + dA_x)
     int4* slot_base = reinterpret_cast<int4*>(smem + L.slots);
     unsigned* twm_base = reinterpret_cast<unsigned*>(smem + L.twm);
     int* zz = reinterpret_cast<int*>(smem + L.zz);
     int* flags = reinterpret_cast<int*>(smem + L.flags);
     unsigned long long* red = reinterpret_cast<unsigned long long*>(smem + L.red);
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + L.bar);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.bar + 8);
     int32_t* D = a.D;
     const uint8_t* Ag = reinterpret_cast<const uint8_t*>(a.A);
     const uint16_t* Bg = reinterpret_cast<const uint16_t*>(a.B);
 
-    // ---- load: A (restrided), tables, σ = id, q = p, B~ = B[q][q], D~ diagonal
-    for (int idx = t; idx < n * lda; idx += RLB_NT) {
-        const int i = idx / lda, j = idx - i * lda;
-        As[idx] = j < ldg ? Ag[i * ldg + j] : (uint8_t)0;
-    }
+    // ---- load: tables, σ = id, q = p
     for (int i = t; i < n; i += RLB_NT) {
         rowaddr[i] = a.rowaddr[i];
         cls[i] = ra.cls[i];
@@ -154,20 +141,43 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
     }
     for (int i = t; i < ncls * (n + 1); i += RLB_NT) pt[i] = ra.pt[i];
     for (int i = t; i < nqt; i += RLB_NT) qdesc[i] = a.qdesc[i];
+    for (int i = t; i < RLB_SBO / 16; i += RLB_NT) reinterpret_cast<uint4*>(op2)[i] = make_uint4(0, 0, 0, 0);
     if (t < 4) flags[t] = 0;
     if (t < 2) red[t] = 0ull;
+    if (t == 0) tc::mbar_init(mbar, 1);
+    if (warp == 0) tc::tmem_alloc(tmem_slot, 32);
+    tc::fence_before_sync();
     __syncthreads();
-    for (int idx = t; idx < n * ldb; idx += RLB_NT) {
-        const int i = idx / ldb, j = idx - i * ldb;
-        Bt[idx] = j < n ? Bg[q[i] * ldg + q[j]] : (uint16_t)0;
+    tc::fence_after_sync();
+    const uint32_t tmem = *tmem_slot;
+    // op1 = [Bh | Bl | A] of the slots: B~ = B[q][q] split into bytes, A (zero beyond n)
+    for (int idx = t; idx < RLB_MAXN * (RLB_K / 4); idx += RLB_NT) {
+        const int x = idx / (RLB_K / 4), k = 4 * (idx - x * (RLB_K / 4));
+        uint32_t w = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int kk = k + e;
+            int v = 0;
+            if (x < n) {
+                if (kk >= RLB_AOFF) { if (kk - RLB_AOFF < n) v = Ag[x * ldg + kk - RLB_AOFF]; }
+                else {
+                    const int c = kk & 255;
+                    if (c < n) {
+                        const int b = Bg[q[x] * ldg + q[c]];
+                        v = kk >= RLB_BL ? (b & 255) : (b >> 8);
+                    }
+                }
+            }
+            w |= (uint32_t)v << (8 * e);
+        }
+        *reinterpret_cast<uint32_t*>(op1 + rlb_off(x, k)) = w;
     }
+    tc::fence_proxy_async();                              // op1 / op2 -> tensor-core operand reads
     __syncthreads();
     for (int x = t; x < n; x += RLB_NT) {
-        const uint4* ax = reinterpret_cast<const uint4*>(As + x * lda);
-        const uint4* bx = reinterpret_cast<const uint4*>(Bt + x * ldb);
-        uint32_t acc = 0;
-        for (int b = 0; b < nb; ++b) acc = dp16w(ax[b], bx[2 * b], bx[2 * b + 1], acc);
-        Dg[x] = (int)acc;
+        int acc = 0;
+        for (int k = 0; k < n; ++k) acc += rlb_A(op1, x, k) * rlb_B(op1, x, k);
+        Dg[x] = acc;
     }
     __syncthreads();
 
@@ -179,7 +189,9 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
     int r, s0;
     tri_pair(n, (int)(k % (uint64_t)M), &r, &s0);
     int parity = 0, pa = -1, pb = -1;
+    uint32_t mma_phase = 0;
     float rejT = 38.5f * temp32(a.sch, k);
+    const uint32_t idesc = tc::idesc_i8(128, 8, false);   // u8 x u8 -> s32, M = 128, N = 8
 
     while (k < k_end) {
         const uint64_t remaining = k_end - k;
@@ -187,25 +199,31 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
 
         // ---- deferred B~ exchange of the last cross accept (slots pa, pb) and best_p
         if (pa >= 0) {
-            for (int x = t; x < n; x += RLB_NT) {
+            for (int x = t; x < n; x += RLB_NT) {        // columns pa, pb of the other rows
                 if (x == pa || x == pb) continue;
-                uint16_t* row = Bt + x * ldb;
-                const uint16_t v = row[pa];
-                row[pa] = row[pb];
-                row[pb] = v;
-            }
-            if (warp == 1) {                              // rows pa, pb, word-wise
-                uint32_t* Rw = reinterpret_cast<uint32_t*>(Bt + pa * ldb);
-                uint32_t* Sw = reinterpret_cast<uint32_t*>(Bt + pb * ldb);
-                for (int w = lane; w < ldb / 2; w += 32) {
-                    uint32_t m = 0;
-                    if (pa / 2 == w) m |= 0xFFFFu << (16 * (pa & 1));
-                    if (pb / 2 == w) m |= 0xFFFFu << (16 * (pb & 1));
-                    const uint32_t x = Rw[w], y = Sw[w];
-                    Rw[w] = (y & ~m) | (x & m);
-                    Sw[w] = (x & ~m) | (y & m);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    uint8_t* ra_ = op1 + rlb_off(x, h * RLB_BL + pa);
+                    uint8_t* rb_ = op1 + rlb_off(x, h * RLB_BL + pb);
+                    const uint8_t v = *ra_;
+                    *ra_ = *rb_;
+                    *rb_ = v;
                 }
             }
+            if (warp == 1) {                              // rows pa, pb (Bh and Bl), word-wise
+                for (int w = lane; w < 2 * RLB_BL / 4; w += 32) {
+                    const int kk = 4 * w, c = kk & 255;
+                    uint32_t m = 0;
+                    if ((unsigned)(pa - c) < 4u) m |= 0xFFu << (8 * (pa - c));
+                    if ((unsigned)(pb - c) < 4u) m |= 0xFFu << (8 * (pb - c));
+                    uint32_t* Rw = reinterpret_cast<uint32_t*>(op1 + rlb_off(pa, kk));
+                    uint32_t* Sw = reinterpret_cast<uint32_t*>(op1 + rlb_off(pb, kk));
+                    const uint32_t x = *Rw, y = *Sw;
+                    *Rw = (y & ~m) | (x & m);             // (pa,pa), (pa,pb), (pb,pa), (pb,pb) keep
+                    *Sw = (x & ~m) | (y & m);             // their values (B~ symmetric, zero diag)
+                }
+            }
+            tc::fence_proxy_async();                      // op1 writes -> next MMA's operand reads
             if (flags[0])
                 for (int x = t; x < n; x += RLB_NT) bestp[x] = q[sig[x]];
             pa = -1;
@@ -279,85 +297,116 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
         const int4 win = slots[j >> 5];
         const int dw = win.y, sa = win.z >> 16, sb = win.z & 0xFFFF, sl = win.w;
         const uint64_t kacc = k + (uint64_t)j;
-        const uint8_t* Aa = As + sa * lda;
-        const uint8_t* Ab = As + sb * lda;
-        const uint16_t* Ba = Bt + sa * ldb;
-        const uint16_t* Bb = Bt + sb * ldb;
-        // stage and Z (the new diagonal of slots a, b)
-        if (t < n) stg[t] = make_int2((int)Aa[t] - (int)Ab[t], (int)Ba[t] - (int)Bb[t]);
+        // stage, Z (the new diagonal of slots a, b), the MMA's B operand W
+        // dA in [-255, 255], dB in [-65535, 65535] packed as 2 (1024 dB + dA): the difference of two
+        // packed values is 2048 (dB_u - dB_v) + 2 (dA_u - dA_v) with |dA_u - dA_v| <= 510, so
+        // hi = (d + 1024) >> 11 and lo2 = d - 2048 hi recover both and lo2 * hi is the rank term
+        if (t < n)
+            stg[t] = 2 * (1024 * (rlb_B(op1, sa, t) - rlb_B(op1, sb, t)) + rlb_A(op1, sa, t) - rlb_A(op1, sb, t));
         if (warp == 8 || warp == 9) {
-            const uint8_t* X = warp == 8 ? Aa : Ab;
-            const uint16_t* Y = warp == 8 ? Bb : Ba;
+            const int X = warp == 8 ? sa : sb, Y = warp == 8 ? sb : sa;
             int z = 0;
-            for (int x = lane; x < n; x += 32) z += (int)X[x] * (int)Y[x];
+            for (int x = lane; x < n; x += 32) z += rlb_A(op1, X, x) * rlb_B(op1, Y, x);
             z = __reduce_add_sync(0xffffffffu, z);
             if (lane == 0) zz[warp - 8] = z;
         }
+        if (t >= 512 && t < 640) {                        // W: 8 columns x 16 chunks of 16 bytes
+            const int col = (t - 512) >> 4, c16 = 16 * ((t - 512) & 15);
+            const int row = (col & 1) ? sb : sa;
+            int ksrc, kdst;
+            if (col < 4) { ksrc = RLB_AOFF + c16; kdst = (col < 2 ? 0 : RLB_BL) + c16; }
+            else { ksrc = (col == 4 || col == 6) ? RLB_BL + c16 : c16; kdst = RLB_AOFF + c16; }
+            const int rowx = col < 4 ? row : ((col < 6) ? sa : sb);
+            *reinterpret_cast<uint4*>(op2 + rlb_off(col, kdst)) =
+                *reinterpret_cast<const uint4*>(op1 + rlb_off(rowx, ksrc));
+            tc::fence_proxy_async();
+        }
         __syncthreads();
-        const int ars = Aa[sb], brs = Ba[sb];
+        const int ars = rlb_A(op1, sa, sb), brs = rlb_B(op1, sa, sb);
         const int Da = zz[0] + ars * brs;                 // D''_a = A_a.B~_b + a_ab B~_ab
         const int Db = zz[1] + ars * brs;
-        if (t < RLB_TOUCH) {
-            // touching entries: 2 threads per v, half of the row blocks each
-            const int v = t >> 1, part = t & 1;
-            int xa = 0, xb = 0, ya = 0, yb = 0;
-            if (v < n) rlb_dots(As + v * lda, Bt + v * ldb, Aa, Ab, Ba, Bb, part, 2, nb, xa, xb, ya, yb);
-            xa += __shfl_xor_sync(0xffffffffu, xa, 1);
-            xb += __shfl_xor_sync(0xffffffffu, xb, 1);
-            ya += __shfl_xor_sync(0xffffffffu, ya, 1);
-            yb += __shfl_xor_sync(0xffffffffu, yb, 1);
-            if (part == 0 && v < n && v != sa && v != sb) {
-                const int av = Aa[v], bv = Ab[v], abv = Ba[v], bbv = Bb[v];
-                const int da = av - bv, db = abv - bbv;
-                const int dv = Dg[v] - da * db;           // D''_v = D_v - dA_v dB_v
-                Dg[v] = dv;
-                // R10b: δ''(a,v) and δ''(b,v) from pre-swap rows
-                D[v > sa ? rowaddr[sa] + v : rowaddr[v] + sa] =
-                    2 * (xa + ars * db + yb - da * brs - Da - dv + 2 * av * bbv);
-                D[v > sb ? rowaddr[sb] + v : rowaddr[v] + sb] =
-                    2 * (xb - ars * db + ya + da * brs - Db - dv + 2 * bv * abv);
-            }
-        } else {
-            // disjoint entries (R10): quads g = qt, qt + 512, ... (consecutive threads read
-            // consecutive 16-byte quads of Δ~, which streams through L2); rows sa, sb skipped,
-            // columns sa, sb left to the touching threads.  RLB_QB loads in flight per thread.
-            const int qt = t - RLB_TOUCH;
-            constexpr int QS = RLB_NT - RLB_TOUCH;
+        // touching dot products on the tensor cores (issued now, read after the quads)
+        if (t == 0) {
+            tc::fence_after_sync();
+            const uint32_t o1 = tc::smem_u32(op1), o2 = tc::smem_u32(op2);
 #pragma unroll 1
-            for (int g0 = qt; g0 < nqt; g0 += RLB_QB * QS) {
-                int4 d4[RLB_QB];
-                uint32_t desc[RLB_QB];
+            for (int c = 0; c < (n + 127) / 128; ++c)
+#pragma unroll 1
+                for (int kk = 0; kk < RLB_K / 32; ++kk)
+                    tc::mma_i8(tmem + 8 * c, tc::smem_desc(o1 + c * 16 * RLB_SBO + kk * 256, 128, RLB_SBO),
+                               tc::smem_desc(o2 + kk * 256, 128, RLB_SBO), idesc, kk > 0);
+            tc::mma_commit(mbar);
+        }
+        __syncwarp();
+        // disjoint entries (R10), every thread: quads g = t, t + 1024, ... (consecutive threads read
+        // consecutive 16-byte quads of Δ~, which streams through L2); rows sa, sb skipped; quads
+        // holding columns sa, sb are written whole here and their two entries overwritten by the
+        // touching stores after the barrier below.  RLB_QB loads in flight per thread.
+#pragma unroll 1
+        for (int g0 = t; g0 < nqt; g0 += RLB_QB * RLB_NT) {
+            int4 d4[RLB_QB];
+            uint32_t dsc[RLB_QB];
 #pragma unroll
-                for (int i = 0; i < RLB_QB; ++i) {
-                    const int g = g0 + i * QS;
-                    desc[i] = g < nqt ? (uint32_t)qdesc[g] : 0xFFFFu;
-                    const int u = desc[i] & 511;
-                    if (desc[i] != 0xFFFFu && u != sa && u != sb)
-                        d4[i] = *reinterpret_cast<const int4*>(D + 4 * g);
-                }
-#pragma unroll
-                for (int i = 0; i < RLB_QB; ++i) {
-                    const int u = desc[i] & 511, v0 = (desc[i] >> 9) << 2;
-                    if (desc[i] == 0xFFFFu || u == sa || u == sb) continue;
-                    const int g = g0 + i * QS;
-                    const int2 pu = stg[u];
-                    const int4 x = *reinterpret_cast<const int4*>(stg + v0);
-                    const int4 y = *reinterpret_cast<const int4*>(stg + v0 + 2);
-                    const int4 nv = make_int4(d4[i].x + 2 * (pu.x - x.x) * (pu.y - x.y),
-                                              d4[i].y + 2 * (pu.x - x.z) * (pu.y - x.w),
-                                              d4[i].z + 2 * (pu.x - y.x) * (pu.y - y.y),
-                                              d4[i].w + 2 * (pu.x - y.z) * (pu.y - y.w));
-                    const unsigned er = (unsigned)(sa - v0), es = (unsigned)(sb - v0);
-                    if (__builtin_expect(er >= 4u && es >= 4u, 1)) {
-                        *reinterpret_cast<int4*>(D + 4 * g) = nv;
-                    } else {                              // column sa or sb in this quad
-                        if (er != 0u && es != 0u) D[4 * g + 0] = nv.x;
-                        if (er != 1u && es != 1u) D[4 * g + 1] = nv.y;
-                        if (er != 2u && es != 2u) D[4 * g + 2] = nv.z;
-                        if (er != 3u && es != 3u) D[4 * g + 3] = nv.w;
-                    }
-                }
+            for (int i = 0; i < RLB_QB; ++i) {
+                const int g = g0 + i * RLB_NT;
+                const uint32_t x = g < nqt ? (uint32_t)qdesc[g] : 0xFFFFu;
+                const int u = x & 511;
+                dsc[i] = (x != 0xFFFFu && u != sa && u != sb) ? x : 0xFFFFu;
+                if (dsc[i] != 0xFFFFu) d4[i] = *reinterpret_cast<const int4*>(D + 4 * g);
             }
+#pragma unroll
+            for (int i = 0; i < RLB_QB; ++i) {
+                if (dsc[i] == 0xFFFFu) continue;
+                const int g = g0 + i * RLB_NT;
+                const int u = dsc[i] & 511, v0 = (dsc[i] >> 9) << 2;
+                const int pu = stg[u];
+                const int4 x = *reinterpret_cast<const int4*>(stg + v0);
+                int4 o = d4[i];
+                int dd = pu - x.x, hi = (dd + 1024) >> 11;
+                o.x += (dd - (hi << 11)) * hi;
+                dd = pu - x.y; hi = (dd + 1024) >> 11;
+                o.y += (dd - (hi << 11)) * hi;
+                dd = pu - x.z; hi = (dd + 1024) >> 11;
+                o.z += (dd - (hi << 11)) * hi;
+                dd = pu - x.w; hi = (dd + 1024) >> 11;
+                o.w += (dd - (hi << 11)) * hi;
+                *reinterpret_cast<int4*>(D + 4 * g) = o;
+            }
+        }
+        // touching entries: warps 0..7, one TMEM lane (= one v) per thread
+        int wa = -1, wb = -1, va = 0, vb = 0;
+        if (t < RLB_EPI) {
+            const int c = warp >> 2, v = 128 * c + 32 * (warp & 3) + lane;
+            if (128 * c < n) {
+                tc::mbar_wait(mbar, mma_phase);
+                tc::fence_after_sync();
+                uint32_t R[8];
+                tc::tmem_ld8(tmem + ((uint32_t)(32 * (warp & 3)) << 16) + 8 * c, R);
+                tc::tmem_wait_ld();
+                if (v < n && v != sa && v != sb) {
+                    const int xa = ((int)R[0] << 8) + (int)R[2];  // X_a = B~_v.A_a
+                    const int xb = ((int)R[1] << 8) + (int)R[3];  // X_b = B~_v.A_b
+                    const int ya = (int)R[4] + ((int)R[5] << 8);  // Y_a = A_v.B~_a
+                    const int yb = (int)R[6] + ((int)R[7] << 8);  // Y_b = A_v.B~_b
+                    const int av = rlb_A(op1, sa, v), bv = rlb_A(op1, sb, v);
+                    const int abv = rlb_B(op1, sa, v), bbv = rlb_B(op1, sb, v);
+                    const int da = av - bv, db = abv - bbv;
+                    const int dv = Dg[v] - da * db;       // D''_v = D_v - dA_v dB_v
+                    Dg[v] = dv;
+                    // R10b: δ''(a,v) and δ''(b,v) from pre-swap rows
+                    wa = v > sa ? rowaddr[sa] + v : rowaddr[v] + sa;
+                    va = 2 * (xa + ars * db + yb - da * brs - Da - dv + 2 * av * bbv);
+                    wb = v > sb ? rowaddr[sb] + v : rowaddr[v] + sb;
+                    vb = 2 * (xb - ars * db + ya + da * brs - Db - dv + 2 * bv * abv);
+                }
+                tc::fence_before_sync();
+            }
+            mma_phase ^= 1;
+        }
+        __syncthreads();                                  // quads written: columns sa, sb next
+        if (wa >= 0) {
+            D[wa] = va;
+            D[wb] = vb;
         }
         if (t == 0) {                                     // scalar state
             const uint16_t x = q[sa];
@@ -393,13 +442,16 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
         atomicAdd(&red[0], my_dig);
         atomicAdd(&red[1], my_cnt);
     }
+    tc::fence_before_sync();
     __syncthreads();
+    tc::fence_after_sync();
+    if (warp == 0) tc::tmem_dealloc(tmem, 32);
     for (int x = t; x < n; x += RLB_NT) {
         a.p[x] = q[sig[x]];
         a.best_p[x] = bestp[x];
     }
     for (int g = t; g < nqt; g += RLB_NT) {
-        const uint32_t desc = a.qdesc[g];
+        const uint32_t desc = qdesc[g];
         const int u = desc & 511, v0 = (desc >> 9) << 2;
         const int su = sig[u];
         int4 o4;
