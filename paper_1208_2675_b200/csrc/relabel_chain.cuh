@@ -48,7 +48,11 @@ constexpr int RLB_NT = 1024;
 constexpr int RLB_MAXN = 256;
 constexpr int RLB_MAXCLS = 4;   // twin classes (>= 2 members) the relabel path handles
 constexpr int RLB_EPI = 256;    // threads [0, 256): MMA issue and touching epilogue (after their quads)
+#ifndef RLB_QB_EXP
 constexpr int RLB_QB = 4;       // quad loads in flight per thread
+#else
+constexpr int RLB_QB = RLB_QB_EXP;
+#endif
 constexpr int RLB_K = 768;      // K of the touching product: Bh | Bl | A
 constexpr int RLB_SBO = RLB_K / 16 * 128;        // 8-row group stride of the canonical layout
 constexpr int RLB_BL = 256, RLB_AOFF = 512;      // K offsets of the Bl and A parts
@@ -106,7 +110,6 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
     const int ldg = a.ld;
     const int M = n * (n - 1) / 2;
     const int nqt = NFIX ? quad_count(NFIX) : a.nqt;
-    const int nq4 = (n + 3) >> 2;                        // 16-byte chunks per row
     const int ncls = ra.ncls;
     const RlbLayout L = rlb_layout(n);
     uint8_t* op1 = smem + L.op1;
@@ -182,7 +185,7 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
     __syncthreads();
 
     const NearSink sink{a.near_count, a.near_k, a.near_dec, a.near_cap};
-    int64_t cost = a.st->cost, best = a.st->best_cost;   // scalar thread (t == 0)
+    int64_t cost = a.st->cost, best = a.st->best_cost;   // scalar thread (t == RLB_NT - 1)
     uint64_t my_dig = 0, my_cnt = 0;                     // this thread's accepts (digest is a sum)
     uint64_t k = a.k0;
     const uint64_t k_end = a.k_end;
@@ -337,6 +340,20 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
                                tc::smem_desc(o2 + kk * 256, 128, RLB_SBO), idesc, kk > 0);
             tc::mma_commit(mbar);
         }
+        if (t == RLB_NT - 1) {                            // scalar state (row sa is off the quads)
+            const uint16_t x = q[sa];
+            q[sa] = q[sb];
+            q[sb] = x;
+            cost += dw;
+            const int improved = cost < best;
+            if (improved) best = cost;
+            flags[0] = improved;
+            my_dig += mix64(mix64(kacc) ^ (((uint64_t)(uint32_t)r << 32) | (uint32_t)sl));
+            ++my_cnt;
+            D[rowaddr[sa] + sb] = -dw;                    // swapping back restores C
+            Dg[sa] = Da;
+            Dg[sb] = Db;
+        }
         __syncwarp();
         // disjoint entries (R10), every thread: quads g = t, t + 1024, ... (consecutive threads read
         // consecutive 16-byte quads of Δ~, which streams through L2); rows sa, sb skipped; quads
@@ -345,20 +362,22 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
 #pragma unroll 1
         for (int g0 = t; g0 < nqt; g0 += RLB_QB * RLB_NT) {
             int4 d4[RLB_QB];
-            uint32_t dsc[RLB_QB];
+            unsigned need = 0;
 #pragma unroll
             for (int i = 0; i < RLB_QB; ++i) {
                 const int g = g0 + i * RLB_NT;
-                const uint32_t x = g < nqt ? (uint32_t)qdesc[g] : 0xFFFFu;
-                const int u = x & 511;
-                dsc[i] = (x != 0xFFFFu && u != sa && u != sb) ? x : 0xFFFFu;
-                if (dsc[i] != 0xFFFFu) d4[i] = *reinterpret_cast<const int4*>(D + 4 * g);
+                const int u = g < nqt ? (qdesc[g] & 511) : sa;
+                if (u != sa && u != sb) {
+                    need |= 1u << i;
+                    d4[i] = *reinterpret_cast<const int4*>(D + 4 * g);
+                }
             }
 #pragma unroll
             for (int i = 0; i < RLB_QB; ++i) {
-                if (dsc[i] == 0xFFFFu) continue;
+                if (!(need & (1u << i))) continue;
                 const int g = g0 + i * RLB_NT;
-                const int u = dsc[i] & 511, v0 = (dsc[i] >> 9) << 2;
+                const uint32_t dsc = qdesc[g];
+                const int u = dsc & 511, v0 = (dsc >> 9) << 2;
                 const int pu = stg[u];
                 const int4 x = *reinterpret_cast<const int4*>(stg + v0);
                 int4 o = d4[i];
@@ -408,20 +427,6 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
             D[wa] = va;
             D[wb] = vb;
         }
-        if (t == 0) {                                     // scalar state
-            const uint16_t x = q[sa];
-            q[sa] = q[sb];
-            q[sb] = x;
-            cost += dw;
-            const int improved = cost < best;
-            if (improved) best = cost;
-            flags[0] = improved;
-            my_dig += mix64(mix64(kacc) ^ (((uint64_t)(uint32_t)r << 32) | (uint32_t)sl));
-            ++my_cnt;
-            D[rowaddr[sa] + sb] = -dw;                    // swapping back restores C
-            Dg[sa] = Da;
-            Dg[sb] = Db;
-        }
         __syncthreads();
         pa = sa;
         pb = sb;
@@ -468,7 +473,7 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
         }
         *reinterpret_cast<int4*>(ra.d_out + 4 * g) = o4;
     }
-    if (t == 0) {
+    if (t == RLB_NT - 1) {
         a.st->cost = cost;
         a.st->best_cost = best;
         a.st->digest = a.st->digest + red[0];
