@@ -314,6 +314,10 @@ def run_ours(args):
     if not args.no_ensemble:
         ens = run_ensemble(args, Q, s, pg, ws, rank, sch_t0tf=(t0, tf))
 
+    cfg4 = None
+    if rank == 0 and not args.no_config4:
+        cfg4 = run_config4(args, Q)
+
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args.cpu_sample)
@@ -343,12 +347,38 @@ def run_ours(args):
         }
         if ens is not None:
             line["ensemble"] = ens
+        if cfg4 is not None:
+            line["config4_prefix"] = cfg4
         print(json.dumps(line), flush=True)
     s.close()
     if pg:
         pg.barrier()
         pg.destroy_process_group()
     return 0
+
+
+def run_config4(args, Q):
+    """BASELINE config 4 (N=256 grey density, 16-bit B, 1e9-iteration schedule): device time of
+    its first args.cfg4_iters iterations on the relabel engine (rank 0, one call, after one
+    warm-up call on a separate context).  A prefix, not the whole run: the schedule's hot start."""
+    A, B, p0, cfg = config(4)
+    I = args.cfg4_iters
+    out = {}
+    for rep in range(2):
+        s4 = Q.Solver(A, B, p0)
+        s4.delta_init()
+        t0, tf = s4.schedule_bounds()
+        sch = Q.make_schedule(Q.QAP_COOL_GEOMETRIC, t0, tf, cfg["iters"])
+        g = s4.run(0, I if rep else min(I, 10**5), sch, SA_SEED)
+        ms, launches = s4.last_kernel_time()
+        eng = s4.engine()
+        s4.close()
+    return {"workload": "config4 tai256c-shaped N=256 (uint16 B), iterations [0, %d) of 1e9" % I,
+            "metric": "SA iterations/s (1 chain, N=256)", "unit": "iterations/s",
+            "value": I / (ms / 1e3), "kernel_ms": ms,
+            "engine": {Q.QAP_ENGINE_RELABEL: "relabel (k_sa_relabel)",
+                       Q.QAP_ENGINE_SHARED_MEMORY: "shared-memory (k_sa_chain)"}.get(eng, str(eng)),
+            "accepted": g["accepted"], "cost": g["cost"], "gpu_launches": launches}
 
 
 def run_ensemble(args, Q, s, pg, ws, rank, sch_t0tf):
@@ -405,6 +435,8 @@ def main():
     ap.add_argument("--ens-chains", type=int, default=8192)
     ap.add_argument("--ens-iters", type=int, default=10**7)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-config4", action="store_true")
+    ap.add_argument("--cfg4-iters", type=int, default=10**6)
     ap.add_argument("--cpu-sample", type=int, default=3 * 10**7)
     ap.add_argument("--ref-sample", type=int, default=10**7)
     args = ap.parse_args()
