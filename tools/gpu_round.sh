@@ -10,7 +10,7 @@ timeout 1500 python -m pytest tests -q -m gpu > $OUT/pytest_gpu.log 2>&1; echo "
 timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?" >> $OUT/bench.err
 timeout 600 python bench.py --impl reference --steps 1 --warmup 0 > $OUT/bench_ref.json 2> $OUT/bench_ref.err
 # launch list of the timed single-chain workload (same command plain, then under ncu)
-CMD="python bench.py --steps 2 --warmup 3 --no-ensemble --no-cpu-baseline --e2e-steps 1"
+CMD="python bench.py --steps 2 --warmup 3 --no-ensemble --no-cpu-baseline --no-config4 --e2e-steps 1"
 timeout 300 $CMD > $OUT/plain.log 2>&1 && \
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file $OUT/launches_$TAG.csv $CMD > $OUT/ncu_launch.log 2>&1
