@@ -190,12 +190,15 @@ typedef enum {
                                     start of each qap_sa_run without Δ (δ from G = A B'^T, SURVEY
                                     f2) until no swap is accepted for 4096 iterations, then rebuild
                                     Δ and continue with Δ; 0 = Δ throughout.  Same trajectory. */
-    QAP_OPT_RELABEL = 7          /* instances with 8-bit A and 16-bit B, 4 <= n <= 256 (config 4):
+    QAP_OPT_RELABEL = 7,         /* instances with 8-bit A and 16-bit B, 4 <= n <= 256 (config 4):
                                     1 (default) = relabel engine: swaps of twin locations (equal
                                     rows of A off the pair, R21) are exact O(1) index
                                     relabels, other swaps the ordinary update;
                                     2 = the same engine with the relabels off; 0 = the
                                     shared-memory kernel.  Same trajectory in every case. */
+    QAP_OPT_RELABEL_CLUSTER = 8  /* relabel engine: 8 (default) = one chain on a thread-block
+                                    cluster of 8 SMs, Δ spread over their shared memory (SURVEY
+                                    f1); 1 = one SM, Δ in L2 */
 } qap_option;
 qap_status qap_set_option(qap_ctx* ctx, int32_t key, int64_t value);
 /* 1 if the next qap_sa_run uses the tensor-memory engine (QAP_OPT_TENSOR_CORE), else 0. */

@@ -61,6 +61,7 @@ struct qap_ctx {
     int last_launches = 0;
     // relabel engine (relabel_chain.cuh): twin classes of A, second Δ buffer for the write-back
     int use_relabel = 1;                // QAP_OPT_RELABEL
+    int rlb_cluster = 8;                // QAP_OPT_RELABEL_CLUSTER: CTAs sharing Δ~ (1 = Δ~ in L2)
     int ncls = 0;
     uint8_t* dcls = nullptr;            // n
     uint16_t* dpt = nullptr;            // ncls x (n+1)
@@ -188,7 +189,7 @@ static void twin_classes(int n, const int32_t* A, std::vector<uint8_t>* cls, std
 
 static bool use_relabel_engine(const qap_ctx* c) {
     return c->use_relabel && c->ta == 1 && c->tb == 2 && c->n >= 4 && c->n <= RLB_MAXN &&
-           rlb_layout(c->n).bytes <= c->smem_optin;
+           rlb_layout(c->n, c->rlb_cluster).bytes <= c->smem_optin;
 }
 
 static qap_status validate_schedule(qap_ctx* c, const qap_schedule* s, uint64_t k0, uint64_t iters,
@@ -502,7 +503,7 @@ qap_status qap_sa_run(qap_ctx* c, uint64_t k0, uint64_t iters, const qap_schedul
     const int threads = tc ? TCK_NT : effective_threads(c, explicit_threads ? c->threads : auto_threads(c));
     bool ds = !c->force_global && chain_smem_bytes(c, threads, true) <= c->smem_optin;
     const int smem = tc ? tc_layout(c->ld).bytes
-                        : rlb ? rlb_layout(c->n).bytes
+                        : rlb ? rlb_layout(c->n, c->rlb_cluster).bytes
                               : chain_smem_bytes(c, threads, ds);
     if (smem > c->smem_optin) return fail(c, QAP_E_UNSUPPORTED, "chain state does not fit on chip");
 
@@ -546,10 +547,23 @@ qap_status qap_sa_run(qap_ctx* c, uint64_t k0, uint64_t iters, const qap_schedul
         ra.pt = c->dpt;
         ra.ncls = c->use_relabel == 2 ? 0 : c->ncls;
         ra.d_out = c->dD2;
-        auto kern = c->n == 256 ? k_sa_relabel<256> : k_sa_relabel<0>;
+        const int CL = c->rlb_cluster;
+        auto kern = CL == 8 ? (c->n == 256 ? k_sa_relabel<256, 8> : k_sa_relabel<0, 8>)
+                            : (c->n == 256 ? k_sa_relabel<256, 1> : k_sa_relabel<0, 1>);
         CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        kern<<<1, RLB_NT, smem, c->stream>>>(ra);
-        CU(cudaGetLastError());
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3(CL, 1, 1);
+        lc.blockDim = dim3(RLB_NT, 1, 1);
+        lc.dynamicSmemBytes = smem;
+        lc.stream = c->stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = CL;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        CU(cudaLaunchKernelEx(&lc, kern, ra));
         std::swap(c->dD, c->dD2);              // Δ in location space is in the second buffer
     } else {
         CU(launch_chain(c, a, threads, explicit_threads, ds, smem));
@@ -792,6 +806,10 @@ qap_status qap_set_option(qap_ctx* c, int32_t key, int64_t value) {
         case QAP_OPT_RELABEL:
             if (value < 0 || value > 2) return fail(c, QAP_E_INVALID_ARG, "relabel must be 0, 1 or 2");
             c->use_relabel = (int)value;
+            return QAP_OK;
+        case QAP_OPT_RELABEL_CLUSTER:
+            if (value != 1 && value != 8) return fail(c, QAP_E_INVALID_ARG, "relabel cluster must be 1 or 8");
+            c->rlb_cluster = (int)value;
             return QAP_OK;
         case QAP_OPT_ENSEMBLE_GROUP:
             if (value != 64 && value != 128 && value != 256) return fail(c, QAP_E_INVALID_ARG, "group must be 64, 128 or 256");

@@ -58,17 +58,22 @@ constexpr int RLB_SBO = RLB_K / 16 * 128;        // 8-row group stride of the ca
 constexpr int RLB_BL = 256, RLB_AOFF = 512;      // K offsets of the Bl and A parts
 
 struct RlbLayout {
-    int op1, op2, rowaddr, qdesc, pt, cls, sig, q, bestp, dg, stg, slots, twm, zz, flags, red, bar,
-        bytes;
+    int op1, op2, dsh, rowaddr, qdesc, pt, cls, sig, q, bestp, dg, stg, slots, twm, zz, flags, red,
+        bar, bytes;
 };
-__host__ __device__ constexpr RlbLayout rlb_layout(int n) {
+// quads of Δ~ owned by each CTA of a cluster of CL (quad g belongs to CTA g % CL)
+__host__ __device__ constexpr int rlb_share(int n, int CL) { return (quad_count(n) + CL - 1) / CL; }
+// CL = 1: Δ~ in global memory, all quad descriptors in shared memory; CL > 1: this CTA's share of
+// Δ~ and of the descriptors in shared memory
+__host__ __device__ constexpr RlbLayout rlb_layout(int n, int CL = 1) {
     RlbLayout L{};
     const int n4 = (n + 3) & ~3;
     int o = 0;
     L.op1 = o;     o += RLB_MAXN / 8 * RLB_SBO;          // 256 rows x 768 B, canonical K-major
     L.op2 = o;     o += RLB_SBO;                        // 8 rows x 768 B
+    L.dsh = o;     o += CL > 1 ? rlb_share(n, CL) * 16 : 0;
     L.rowaddr = o; o = align16(o + n * 4);
-    L.qdesc = o;   o = align16(o + quad_count(n) * 2);
+    L.qdesc = o;   o = align16(o + (CL > 1 ? rlb_share(n, CL) : quad_count(n)) * 2);
     L.pt = o;      o = align16(o + RLB_MAXCLS * (n + 1) * 2);
     L.cls = o;     o = align16(o + n4);
     L.sig = o;     o = align16(o + n * 2);
@@ -101,7 +106,27 @@ __device__ __forceinline__ int rlb_B(const uint8_t* op1, int x, int k) {
     return ((int)op1[rlb_off(x, k)] << 8) | (int)op1[rlb_off(x, RLB_BL + k)];
 }
 
-template <int NFIX>
+// ---- thread-block cluster helpers (f1: Δ~ spread over the shared memory of CL CTAs)
+__device__ __forceinline__ int cl_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return (int)r;
+}
+__device__ __forceinline__ void cl_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cl_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+__device__ __forceinline__ int cl_load(const int32_t* local, int rank) {   // *local in CTA `rank`
+    uint32_t ra, v;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(tc::smem_u32(local)), "r"(rank));
+    asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(ra) : "memory");
+    return (int)v;
+}
+
+// CL = 1: one CTA, Δ~ in global memory / L2.  CL > 1 (launched as a cluster of CL CTAs): every
+// CTA runs the same chain (same decisions, replicated σ, q, B~, stage and touching products) but
+// owns only the quads g with g % CL == its rank, in shared memory; window reads of other CTAs'
+// quads go through distributed shared memory; two split cluster barriers per non-twin accept
+// (reads of the window done -> writes of the update; writes done -> next window's reads).
+template <int NFIX, int CL>
 __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) {
     extern __shared__ __align__(16) unsigned char smem[];
     const ChainArgs& a = ra.c;
@@ -111,7 +136,10 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
     const int M = n * (n - 1) / 2;
     const int nqt = NFIX ? quad_count(NFIX) : a.nqt;
     const int ncls = ra.ncls;
-    const RlbLayout L = rlb_layout(n);
+    const RlbLayout L = rlb_layout(n, CL);
+    const int crank = CL > 1 ? cl_rank() : 0;
+    const int nql = CL > 1 ? (nqt - crank + CL - 1) / CL : nqt;   // quads this CTA owns
+    int32_t* Ds = reinterpret_cast<int32_t*>(smem + L.dsh);       // CL > 1: local share of Δ~
     uint8_t* op1 = smem + L.op1;
     uint8_t* op2 = smem + L.op2;
     int32_t* rowaddr = reinterpret_cast<int32_t*>(smem + L.rowaddr);
@@ -143,7 +171,10 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
         bestp[i] = (uint16_t)a.best_p[i];
     }
     for (int i = t; i < ncls * (n + 1); i += RLB_NT) pt[i] = ra.pt[i];
-    for (int i = t; i < nqt; i += RLB_NT) qdesc[i] = a.qdesc[i];
+    for (int i = t; i < nql; i += RLB_NT) qdesc[i] = a.qdesc[CL > 1 ? crank + CL * i : i];
+    if (CL > 1)
+        for (int i = t; i < nql; i += RLB_NT)
+            reinterpret_cast<int4*>(Ds)[i] = reinterpret_cast<const int4*>(a.D)[crank + CL * i];
     for (int i = t; i < RLB_SBO / 16; i += RLB_NT) reinterpret_cast<uint4*>(op2)[i] = make_uint4(0, 0, 0, 0);
     if (t < 4) flags[t] = 0;
     if (t < 2) red[t] = 0ull;
@@ -183,7 +214,21 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
         Dg[x] = acc;
     }
     __syncthreads();
+    if (CL > 1) { cl_arrive(); cl_wait(); }               // every CTA's share loaded
 
+    // Δ~ entry e (int index of the quad layout): read (any CTA's share), write (owner only)
+    auto drd = [&](int e) -> int {
+        if (CL == 1) return D[e];
+        const int g = e >> 2, own = g % CL;
+        const int32_t* loc = Ds + 4 * (g / CL) + (e & 3);
+        return own == crank ? *loc : cl_load(loc, own);
+    };
+    auto dwr = [&](int e, int v) {
+        if (CL == 1) { D[e] = v; return; }
+        const int g = e >> 2;
+        if (g % CL == crank) Ds[4 * (g / CL) + (e & 3)] = v;
+    };
+    bool pend_wait = false;                               // CL > 1: writes of the last update
     const NearSink sink{a.near_count, a.near_k, a.near_dec, a.near_cap};
     int64_t cost = a.st->cost, best = a.st->best_cost;   // scalar thread (t == RLB_NT - 1)
     uint64_t my_dig = 0, my_cnt = 0;                     // this thread's accepts (digest is a sum)
@@ -232,6 +277,7 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
             pa = -1;
         }
 
+        if (CL > 1 && pend_wait) { cl_wait(); pend_wait = false; }   // other CTAs' updates visible
         // ---- window: candidates (r, s0 + t), t < Wl
         const int cr = ncls ? cls[r] : 0xFF;
         bool acc = false, near = false, twin = false;
@@ -247,7 +293,7 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
                 const int ss = sig[s];
                 const int sa = min(sr, ss), sb = max(sr, ss);
                 sab = (sa << 16) | sb;
-                d = D[rowaddr[sa] + sb];
+                d = drd(rowaddr[sa] + sb);
                 if (d <= 0) {
                     acc = true;                           // δ < 0, or δ = 0: exp(0) = 1 > r (R5)
                 } else if ((float)d <= rejT) {            // else certain reject (chain.cuh)
@@ -273,7 +319,7 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
         const int lo = cons - 32 * lane;
         const unsigned below = lo >= 32 ? 0xffffffffu : (lo <= 0 ? 0u : ((1u << lo) - 1u));
         const bool any_twin = __reduce_or_sync(0xffffffffu, twm[lane] & below) != 0u;
-        if (near && t < cons) {                           // R16: near ties of consumed iterations
+        if (near && t < cons && crank == 0) {             // R16: near ties of consumed iterations
             const unsigned int i = atomicAdd(sink.count, 1u);
             if ((int)i < sink.cap) {
                 sink.ks[i] = (unsigned long long)(k + (uint64_t)t);
@@ -284,8 +330,10 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
             const uint16_t old = sig[s];
             sig[s] = newsig;
             if (pt[cr * (n + 1) + s0 + cons] == s) sig[r] = old;   // last consumed twin
-            ++my_cnt;
-            my_dig += mix64(mix64(k + (uint64_t)t) ^ (((uint64_t)(uint32_t)r << 32) | (uint32_t)s));
+            if (crank == 0) {
+                ++my_cnt;
+                my_dig += mix64(mix64(k + (uint64_t)t) ^ (((uint64_t)(uint32_t)r << 32) | (uint32_t)s));
+            }
         }
         if (j == INT_MAX) {                               // no cross accept in the window
             k += (uint64_t)cons;
@@ -297,6 +345,7 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
         }
 
         // ---- cross accept: slots (sa, sb), location pair (r, sl)
+        if (CL > 1) cl_arrive();                          // this CTA's window reads are done
         const int4 win = slots[j >> 5];
         const int dw = win.y, sa = win.z >> 16, sb = win.z & 0xFFFF, sl = win.w;
         const uint64_t kacc = k + (uint64_t)j;
@@ -348,39 +397,26 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
             const int improved = cost < best;
             if (improved) best = cost;
             flags[0] = improved;
-            my_dig += mix64(mix64(kacc) ^ (((uint64_t)(uint32_t)r << 32) | (uint32_t)sl));
-            ++my_cnt;
-            D[rowaddr[sa] + sb] = -dw;                    // swapping back restores C
+            if (crank == 0) {
+                my_dig += mix64(mix64(kacc) ^ (((uint64_t)(uint32_t)r << 32) | (uint32_t)sl));
+                ++my_cnt;
+            }
             Dg[sa] = Da;
             Dg[sb] = Db;
         }
         __syncwarp();
-        // disjoint entries (R10), every thread: quads g = t, t + 1024, ... (consecutive threads read
-        // consecutive 16-byte quads of Δ~, which streams through L2); rows sa, sb skipped; quads
-        // holding columns sa, sb are written whole here and their two entries overwritten by the
-        // touching stores after the barrier below.  RLB_QB loads in flight per thread.
+        if (CL > 1) cl_wait();                            // every CTA done reading this window
+        if (CL > 1) {
+            // disjoint entries (R10) of this CTA's share, in shared memory
+            int4* D4 = reinterpret_cast<int4*>(Ds);
 #pragma unroll 1
-        for (int g0 = t; g0 < nqt; g0 += RLB_QB * RLB_NT) {
-            int4 d4[RLB_QB];
-            unsigned need = 0;
-#pragma unroll
-            for (int i = 0; i < RLB_QB; ++i) {
-                const int g = g0 + i * RLB_NT;
-                const int u = g < nqt ? (qdesc[g] & 511) : sa;
-                if (u != sa && u != sb) {
-                    need |= 1u << i;
-                    d4[i] = *reinterpret_cast<const int4*>(D + 4 * g);
-                }
-            }
-#pragma unroll
-            for (int i = 0; i < RLB_QB; ++i) {
-                if (!(need & (1u << i))) continue;
-                const int g = g0 + i * RLB_NT;
-                const uint32_t dsc = qdesc[g];
+            for (int li = t; li < nql; li += RLB_NT) {
+                const uint32_t dsc = qdesc[li];
                 const int u = dsc & 511, v0 = (dsc >> 9) << 2;
+                if (u == sa || u == sb) continue;
                 const int pu = stg[u];
                 const int4 x = *reinterpret_cast<const int4*>(stg + v0);
-                int4 o = d4[i];
+                int4 o = D4[li];
                 int dd = pu - x.x, hi = (dd + 1024) >> 11;
                 o.x += (dd - (hi << 11)) * hi;
                 dd = pu - x.y; hi = (dd + 1024) >> 11;
@@ -389,7 +425,45 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
                 o.z += (dd - (hi << 11)) * hi;
                 dd = pu - x.w; hi = (dd + 1024) >> 11;
                 o.w += (dd - (hi << 11)) * hi;
-                *reinterpret_cast<int4*>(D + 4 * g) = o;
+                D4[li] = o;
+            }
+        } else {
+            // disjoint entries (R10), every thread: quads g = t, t + 1024, ... (consecutive threads read
+            // consecutive 16-byte quads of Δ~, which streams through L2); rows sa, sb skipped; quads
+            // holding columns sa, sb are written whole here and their two entries overwritten by the
+            // touching stores after the barrier below.  RLB_QB loads in flight per thread.
+    #pragma unroll 1
+            for (int g0 = t; g0 < nqt; g0 += RLB_QB * RLB_NT) {
+                int4 d4[RLB_QB];
+                unsigned need = 0;
+    #pragma unroll
+                for (int i = 0; i < RLB_QB; ++i) {
+                    const int g = g0 + i * RLB_NT;
+                    const int u = g < nqt ? (qdesc[g] & 511) : sa;
+                    if (u != sa && u != sb) {
+                        need |= 1u << i;
+                        d4[i] = *reinterpret_cast<const int4*>(D + 4 * g);
+                    }
+                }
+    #pragma unroll
+                for (int i = 0; i < RLB_QB; ++i) {
+                    if (!(need & (1u << i))) continue;
+                    const int g = g0 + i * RLB_NT;
+                    const uint32_t dsc = qdesc[g];
+                    const int u = dsc & 511, v0 = (dsc >> 9) << 2;
+                    const int pu = stg[u];
+                    const int4 x = *reinterpret_cast<const int4*>(stg + v0);
+                    int4 o = d4[i];
+                    int dd = pu - x.x, hi = (dd + 1024) >> 11;
+                    o.x += (dd - (hi << 11)) * hi;
+                    dd = pu - x.y; hi = (dd + 1024) >> 11;
+                    o.y += (dd - (hi << 11)) * hi;
+                    dd = pu - x.z; hi = (dd + 1024) >> 11;
+                    o.z += (dd - (hi << 11)) * hi;
+                    dd = pu - x.w; hi = (dd + 1024) >> 11;
+                    o.w += (dd - (hi << 11)) * hi;
+                    *reinterpret_cast<int4*>(D + 4 * g) = o;
+                }
             }
         }
         // touching entries: warps 0..7, one TMEM lane (= one v) per thread
@@ -424,10 +498,12 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
         }
         __syncthreads();                                  // quads written: columns sa, sb next
         if (wa >= 0) {
-            D[wa] = va;
-            D[wb] = vb;
+            dwr(wa, va);
+            dwr(wb, vb);
         }
+        if (t == RLB_NT - 1) dwr(rowaddr[sa] + sb, -dw);  // swapping back restores C
         __syncthreads();
+        if (CL > 1) { cl_arrive(); pend_wait = true; }    // this CTA's update written
         pa = sa;
         pb = sb;
         k = kacc + 1;
@@ -437,6 +513,15 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
     }
     if (pa >= 0 && flags[0])
         for (int x = t; x < n; x += RLB_NT) bestp[x] = q[sig[x]];
+    if (CL > 1) {
+        // every CTA's share back to global memory (slot space), visible to the whole cluster
+        if (pend_wait) cl_wait();
+        for (int li = t; li < nql; li += RLB_NT)
+            reinterpret_cast<int4*>(D)[crank + CL * li] = reinterpret_cast<const int4*>(Ds)[li];
+        __threadfence();
+        cl_arrive();
+        cl_wait();
+    }
 
     // ---- write back in location space: p = q∘σ, Δ(u,v) = Δ~(σu, σv)
     for (int o = 16; o; o >>= 1) {
@@ -451,12 +536,13 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
     __syncthreads();
     tc::fence_after_sync();
     if (warp == 0) tc::tmem_dealloc(tmem, 32);
-    for (int x = t; x < n; x += RLB_NT) {
-        a.p[x] = q[sig[x]];
-        a.best_p[x] = bestp[x];
-    }
-    for (int g = t; g < nqt; g += RLB_NT) {
-        const uint32_t desc = qdesc[g];
+    if (crank == 0)
+        for (int x = t; x < n; x += RLB_NT) {
+            a.p[x] = q[sig[x]];
+            a.best_p[x] = bestp[x];
+        }
+    for (int g = crank * RLB_NT + t; g < nqt; g += CL * RLB_NT) {
+        const uint32_t desc = CL > 1 ? (uint32_t)a.qdesc[g] : (uint32_t)qdesc[g];
         const int u = desc & 511, v0 = (desc >> 9) << 2;
         const int su = sig[u];
         int4 o4;
@@ -467,13 +553,13 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
             int val = 0;
             if (v > u && v < n) {
                 const int sv = sig[v];
-                val = D[su < sv ? rowaddr[su] + sv : rowaddr[sv] + su];
+                val = __ldcg(D + (su < sv ? rowaddr[su] + sv : rowaddr[sv] + su));
             }
             o[e] = val;
         }
         *reinterpret_cast<int4*>(ra.d_out + 4 * g) = o4;
     }
-    if (t == RLB_NT - 1) {
+    if (t == RLB_NT - 1 && crank == 0) {
         a.st->cost = cost;
         a.st->best_cost = best;
         a.st->digest = a.st->digest + red[0];

@@ -25,6 +25,7 @@ QAP_OPT_WINDOW_MAX, QAP_OPT_THREADS, QAP_OPT_FORCE_GLOBAL_DELTA, QAP_OPT_ENSEMBL
 QAP_OPT_TENSOR_CORE = 5
 QAP_OPT_SCRATCH_PHASE = 6
 QAP_OPT_RELABEL = 7
+QAP_OPT_RELABEL_CLUSTER = 8
 QAP_ENGINE_SHARED_MEMORY, QAP_ENGINE_TENSOR_MEMORY, QAP_ENGINE_RELABEL = 0, 1, 2
 QAP_NEAR_LOG_CAP = 1024
 

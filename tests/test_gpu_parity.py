@@ -25,7 +25,9 @@ ENGINES = [pytest.param([(TC, 1), (SCR, 1)], id="tmem"), pytest.param([(TC, 1), 
 RLB = Q.QAP_OPT_RELABEL
 # instances with 8-bit A and 16-bit B (config 4): the relabel engine, the same engine with the
 # twin relabels off, the shared-memory engine
+RLBC = Q.QAP_OPT_RELABEL_CLUSTER
 RELABEL_ENGINES = [pytest.param([(RLB, 1)], id="relabel"), pytest.param([(RLB, 2)], id="wide"),
+                   pytest.param([(RLB, 1), (RLBC, 1)], id="relabel_1sm"),
                    pytest.param([(RLB, 0)], id="smem")]
 
 
@@ -292,7 +294,7 @@ def test_relabel_engine_selection():
                                                 (64, [20, 10, 6, 3], 4, 100000),
                                                 (130, [40, 30, 2], 5, 60000),
                                                 (256, [92, 100, 3], 6, 60000)])
-@pytest.mark.parametrize("engine", RELABEL_ENGINES[:2])
+@pytest.mark.parametrize("engine", RELABEL_ENGINES[:3])
 def test_relabel_engine_twin_classes(n, sizes, seed, iters, engine):
     """Instances with twin classes (R21) and 16-bit B: Δ, p, best_p, C, digest and every
     counter bit-exact against the oracle in DELTA mode, relabels on and off."""
@@ -302,7 +304,7 @@ def test_relabel_engine_twin_classes(n, sizes, seed, iters, engine):
     _compare_run(A, B, p0, iters, sch, opts=engine)
 
 
-@pytest.mark.parametrize("engine", RELABEL_ENGINES[:2])
+@pytest.mark.parametrize("engine", RELABEL_ENGINES[:3])
 def test_relabel_engine_no_twins_and_resume(engine):
     """A 16-bit instance without twins (the wide engine's ordinary path), and a twin instance
     split into uneven calls (σ is folded back into p and Δ at every exit)."""
