@@ -19,14 +19,15 @@
 // thread adds its accept to a private count and digest (R18 is a sum).
 //
 // Per cross accept (slots a < b), 1024 threads:
-//   stage   dA_x = A_ax - A_bx, dB_x = B~_ax - B~_bx; Z_a = A_a.B~_b, Z_b = A_b.B~_a (warps 8, 9);
-//           the 8 columns of the MMA's B operand from rows a, b (threads 0..127)
+//   stage   dA_x = A_ax - A_bx, dB_x = B~_ax - B~_bx; the 8 columns of the MMA's B operand from
+//           rows a, b (threads 512..639)
 //   touch   the four dot products of every v, X_a = B~_v.A_a, X_b, Y_a = A_v.B~_a, Y_b, are two
 //           GEMVs: ONE tensor-core product [Bh | Bl | A] (256 x 768, u8) x W (768 x 8, u8), with
 //           B~ = 256 Bh + Bl split into bytes and W's columns (A_a;0;0), (A_b;0;0), (0;A_a;0),
 //           (0;A_b;0), (0;0;Bl_a), (0;0;Bh_a), (0;0;Bl_b), (0;0;Bh_b): 2 x 24 tcgen05.mma
 //           (kind::i8, M = 128, N = 8, K = 32, s32 in TMEM, exact).  Warps 0..7 read the
-//           result (one TMEM lane per v) and write δ''(a,v), δ''(b,v) (R10b) and D~_v
+//           result (one TMEM lane per v; rows a, b of it give Z_a = A_a.B~_b, Z_b = A_b.B~_a, the
+//           new diagonal) and write δ''(a,v), δ''(b,v) (R10b) and D~_v
 //   quads   all threads while the MMAs run: Δ~ += 2(dA_u - dA_v)(dB_u - dB_v) for every pair
 //           off rows a, b (R10), one 16-byte quad at a time; Δ~ in global memory / L2
 //   next window: B~ rows / columns a, b exchanged, best_p = q∘σ if the cost improved
@@ -104,6 +105,16 @@ __device__ __forceinline__ int rlb_off(int x, int k) { return tc::kmaj_off(x, k,
 __device__ __forceinline__ int rlb_A(const uint8_t* op1, int x, int k) { return op1[rlb_off(x, RLB_AOFF + k)]; }
 __device__ __forceinline__ int rlb_B(const uint8_t* op1, int x, int k) {
     return ((int)op1[rlb_off(x, k)] << 8) | (int)op1[rlb_off(x, RLB_BL + k)];
+}
+
+// D[tmem] (+)= A[smem] x B[smem]^T with a compile-time accumulate flag (straight-line issue)
+template <bool ACC>
+__device__ __forceinline__ void rlb_mma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "n"(ACC ? 1 : 0)
+        : "memory");
 }
 
 // ---- thread-block cluster helpers (f1: Δ~ spread over the shared memory of CL CTAs)
@@ -355,13 +366,6 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
         // hi = (d + 1024) >> 11 and lo2 = d - 2048 hi recover both and lo2 * hi is the rank term
         if (t < n)
             stg[t] = 2 * (1024 * (rlb_B(op1, sa, t) - rlb_B(op1, sb, t)) + rlb_A(op1, sa, t) - rlb_A(op1, sb, t));
-        if (warp == 8 || warp == 9) {
-            const int X = warp == 8 ? sa : sb, Y = warp == 8 ? sb : sa;
-            int z = 0;
-            for (int x = lane; x < n; x += 32) z += rlb_A(op1, X, x) * rlb_B(op1, Y, x);
-            z = __reduce_add_sync(0xffffffffu, z);
-            if (lane == 0) zz[warp - 8] = z;
-        }
         if (t >= 512 && t < 640) {                        // W: 8 columns x 16 chunks of 16 bytes
             const int col = (t - 512) >> 4, c16 = 16 * ((t - 512) & 15);
             const int row = (col & 1) ? sb : sa;
@@ -375,18 +379,20 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
         }
         __syncthreads();
         const int ars = rlb_A(op1, sa, sb), brs = rlb_B(op1, sa, sb);
-        const int Da = zz[0] + ars * brs;                 // D''_a = A_a.B~_b + a_ab B~_ab
-        const int Db = zz[1] + ars * brs;
         // touching dot products on the tensor cores (issued now, read after the quads)
         if (t == 0) {
+            // descriptors advance by 256 bytes (one K = 32 step) = 16 in the address field
             tc::fence_after_sync();
-            const uint32_t o1 = tc::smem_u32(op1), o2 = tc::smem_u32(op2);
-#pragma unroll 1
-            for (int c = 0; c < (n + 127) / 128; ++c)
-#pragma unroll 1
-                for (int kk = 0; kk < RLB_K / 32; ++kk)
-                    tc::mma_i8(tmem + 8 * c, tc::smem_desc(o1 + c * 16 * RLB_SBO + kk * 256, 128, RLB_SBO),
-                               tc::smem_desc(o2 + kk * 256, 128, RLB_SBO), idesc, kk > 0);
+            const uint64_t bd = tc::smem_desc(tc::smem_u32(op2), 128, RLB_SBO);
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                if (c == 1 && n <= 128) break;
+                const uint64_t ad = tc::smem_desc(tc::smem_u32(op1) + c * 16 * RLB_SBO, 128, RLB_SBO);
+                rlb_mma<false>(tmem + 8 * c, ad, bd, idesc);
+#pragma unroll
+                for (int kk = 1; kk < RLB_K / 32; ++kk)
+                    rlb_mma<true>(tmem + 8 * c, ad + 16 * kk, bd + 16 * kk, idesc);
+            }
             tc::mma_commit(mbar);
         }
         if (t == RLB_NT - 1) {                            // scalar state (row sa is off the quads)
@@ -401,8 +407,6 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
                 my_dig += mix64(mix64(kacc) ^ (((uint64_t)(uint32_t)r << 32) | (uint32_t)sl));
                 ++my_cnt;
             }
-            Dg[sa] = Da;
-            Dg[sb] = Db;
         }
         __syncwarp();
         if (CL > 1) cl_wait();                            // every CTA done reading this window
@@ -470,12 +474,23 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
         int wa = -1, wb = -1, va = 0, vb = 0;
         if (t < RLB_EPI) {
             const int c = warp >> 2, v = 128 * c + 32 * (warp & 3) + lane;
-            if (128 * c < n) {
+            const bool tile = 128 * c < n;
+            uint32_t R[8];
+            if (tile) {
                 tc::mbar_wait(mbar, mma_phase);
                 tc::fence_after_sync();
-                uint32_t R[8];
                 tc::tmem_ld8(tmem + ((uint32_t)(32 * (warp & 3)) << 16) + 8 * c, R);
                 tc::tmem_wait_ld();
+                // Z_a = A_a.B~_b = Y_b(a) and Z_b = A_b.B~_a = Y_a(b): the new diagonal of a, b
+                if (v == sa) zz[0] = (int)R[6] + ((int)R[7] << 8);
+                if (v == sb) zz[1] = (int)R[4] + ((int)R[5] << 8);
+            }
+            group_sync(1, RLB_EPI);
+            const int Da = zz[0] + ars * brs;             // D''_a = A_a.B~_b + a_ab B~_ab
+            const int Db = zz[1] + ars * brs;
+            if (tile) {
+                if (v == sa) Dg[sa] = Da;
+                if (v == sb) Dg[sb] = Db;
                 if (v < n && v != sa && v != sb) {
                     const int xa = ((int)R[0] << 8) + (int)R[2];  // X_a = B~_v.A_a
                     const int xb = ((int)R[1] << 8) + (int)R[3];  // X_b = B~_v.A_b
