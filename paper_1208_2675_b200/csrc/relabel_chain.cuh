@@ -19,15 +19,15 @@
 // thread adds its accept to a private count and digest (R18 is a sum).
 //
 // Per cross accept (slots a < b), 1024 threads:
-//   stage   dA_x = A_ax - A_bx, dB_x = B~_ax - B~_bx; the 8 columns of the MMA's B operand from
-//           rows a, b (threads 512..639)
+//   stage   dA_x = A_ax - A_bx, dB_x = B~_ax - B~_bx, D''_x = D_x - dA_x dB_x; Z_a = A_a.B~_b,
+//           Z_b = A_b.B~_a (warps 8..15); the 8 columns of the MMA's B operand (threads 512..639)
 //   touch   the four dot products of every v, X_a = B~_v.A_a, X_b, Y_a = A_v.B~_a, Y_b, are two
 //           GEMVs: ONE tensor-core product [Bh | Bl | A] (256 x 768, u8) x W (768 x 8, u8), with
 //           B~ = 256 Bh + Bl split into bytes and W's columns (A_a;0;0), (A_b;0;0), (0;A_a;0),
 //           (0;A_b;0), (0;0;Bl_a), (0;0;Bh_a), (0;0;Bl_b), (0;0;Bh_b): 2 x 24 tcgen05.mma
 //           (kind::i8, M = 128, N = 8, K = 32, s32 in TMEM, exact).  Warps 0..7 read the
-//           result (one TMEM lane per v; rows a, b of it give Z_a = A_a.B~_b, Z_b = A_b.B~_a, the
-//           new diagonal) and write δ''(a,v), δ''(b,v) (R10b) and D~_v
+//           result (one TMEM lane per v) and write δ''(a,v), δ''(b,v) (R10b); on a cluster CTAs 0
+//           and 1 compute one 128-row tile each and store every entry into its owner's share
 //   quads   all threads while the MMAs run: Δ~ += 2(dA_u - dA_v)(dB_u - dB_v) for every pair
 //           off rows a, b (R10), one 16-byte quad at a time; Δ~ in global memory / L2
 //   next window: B~ rows / columns a, b exchanged, best_p = q∘σ if the cost improved
@@ -84,7 +84,7 @@ __host__ __device__ constexpr RlbLayout rlb_layout(int n, int CL = 1) {
     L.stg = o;     o = align16(o + n4 * 4);
     L.slots = o;   o = align16(o + 2 * 32 * 16);
     L.twm = o;     o = align16(o + 2 * 32 * 4);
-    L.zz = o;      o = align16(o + 4 * 4);
+    L.zz = o;      o = align16(o + 16 * 4);
     L.flags = o;   o = align16(o + 4 * 4);
     L.red = o;     o = align16(o + 2 * 8);
     L.bar = o;     o = align16(o + 16);                 // mbarrier + TMEM base address
@@ -125,6 +125,11 @@ __device__ __forceinline__ int cl_rank() {
 }
 __device__ __forceinline__ void cl_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
 __device__ __forceinline__ void cl_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cl_store(int32_t* local, int rank, int v) {  // *local in CTA `rank` = v
+    uint32_t ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(tc::smem_u32(local)), "r"(rank));
+    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(ra), "r"(v) : "memory");
+}
 __device__ __forceinline__ int cl_load(const int32_t* local, int rank) {   // *local in CTA `rank`
     uint32_t ra, v;
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(tc::smem_u32(local)), "r"(rank));
@@ -234,10 +239,17 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
         const int32_t* loc = Ds + 4 * (g / CL) + (e & 3);
         return own == crank ? *loc : cl_load(loc, own);
     };
-    auto dwr = [&](int e, int v) {
+    auto dwr = [&](int e, int v) {                        // replicated value: owner stores
         if (CL == 1) { D[e] = v; return; }
         const int g = e >> 2;
         if (g % CL == crank) Ds[4 * (g / CL) + (e & 3)] = v;
+    };
+    auto dput = [&](int e, int v) {                       // value computed by this CTA only
+        if (CL == 1) { D[e] = v; return; }
+        const int g = e >> 2, own = g % CL;
+        int32_t* loc = Ds + 4 * (g / CL) + (e & 3);
+        if (own == crank) *loc = v;
+        else cl_store(loc, own, v);
     };
     bool pend_wait = false;                               // CL > 1: writes of the last update
     const NearSink sink{a.near_count, a.near_k, a.near_dec, a.near_cap};
@@ -364,8 +376,22 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
         // dA in [-255, 255], dB in [-65535, 65535] packed as 2 (1024 dB + dA): the difference of two
         // packed values is 2048 (dB_u - dB_v) + 2 (dA_u - dA_v) with |dA_u - dA_v| <= 510, so
         // hi = (d + 1024) >> 11 and lo2 = d - 2048 hi recover both and lo2 * hi is the rank term
-        if (t < n)
-            stg[t] = 2 * (1024 * (rlb_B(op1, sa, t) - rlb_B(op1, sb, t)) + rlb_A(op1, sa, t) - rlb_A(op1, sb, t));
+        if (t < n) {
+            const int da = rlb_A(op1, sa, t) - rlb_A(op1, sb, t), db = rlb_B(op1, sa, t) - rlb_B(op1, sb, t);
+            stg[t] = 2 * (1024 * db + da);
+            if (t != sa && t != sb) Dg[t] -= da * db;     // D''_v = D_v - dA_v dB_v (R10b)
+        }
+        if (t >= 256 && t < 512) {                        // Z_a = A_a.B~_b, Z_b = A_b.B~_a (R10b)
+            const int i = t - 256;
+            int za = 0, zb = 0;
+            if (i < n) {
+                za = rlb_A(op1, sa, i) * rlb_B(op1, sb, i);
+                zb = rlb_A(op1, sb, i) * rlb_B(op1, sa, i);
+            }
+            za = __reduce_add_sync(0xffffffffu, za);
+            zb = __reduce_add_sync(0xffffffffu, zb);
+            if (lane == 0) { zz[2 * (warp - 8)] = za; zz[2 * (warp - 8) + 1] = zb; }
+        }
         if (t >= 512 && t < 640) {                        // W: 8 columns x 16 chunks of 16 bytes
             const int col = (t - 512) >> 4, c16 = 16 * ((t - 512) & 15);
             const int row = (col & 1) ? sb : sa;
@@ -379,14 +405,22 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
         }
         __syncthreads();
         const int ars = rlb_A(op1, sa, sb), brs = rlb_B(op1, sa, sb);
+        int Da = ars * brs, Db = ars * brs;               // D''_a = A_a.B~_b + a_ab B~_ab, D''_b
+#pragma unroll
+        for (int w = 0; w < 8; ++w) { Da += zz[2 * w]; Db += zz[2 * w + 1]; }
+        // tiles of the touching product this CTA computes: both on one SM; on a cluster, CTA c
+        // computes rows [128c, 128c + 128) (c < 2) and stores each touching entry to its owner
+        const int ntile = (n + 127) / 128;
+        const bool mine = CL == 1 || crank < ntile;
         // touching dot products on the tensor cores (issued now, read after the quads)
-        if (t == 0) {
+        if (t == 0 && mine) {
             // descriptors advance by 256 bytes (one K = 32 step) = 16 in the address field
             tc::fence_after_sync();
             const uint64_t bd = tc::smem_desc(tc::smem_u32(op2), 128, RLB_SBO);
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
                 if (c == 1 && n <= 128) break;
+                if (CL > 1 && c != crank) continue;
                 const uint64_t ad = tc::smem_desc(tc::smem_u32(op1) + c * 16 * RLB_SBO, 128, RLB_SBO);
                 rlb_mma<false>(tmem + 8 * c, ad, bd, idesc);
 #pragma unroll
@@ -407,6 +441,8 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
                 my_dig += mix64(mix64(kacc) ^ (((uint64_t)(uint32_t)r << 32) | (uint32_t)sl));
                 ++my_cnt;
             }
+            Dg[sa] = Da;
+            Dg[sb] = Db;
         }
         __syncwarp();
         if (CL > 1) cl_wait();                            // every CTA done reading this window
@@ -429,7 +465,18 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
                 o.z += (dd - (hi << 11)) * hi;
                 dd = pu - x.w; hi = (dd + 1024) >> 11;
                 o.w += (dd - (hi << 11)) * hi;
-                D4[li] = o;
+                // columns sa, sb are the touching entries, stored (possibly by another CTA,
+                // unordered with this store) after the quads: leave them alone
+                const unsigned er = (unsigned)(sa - v0), es = (unsigned)(sb - v0);
+                if (er >= 4u && es >= 4u) {
+                    D4[li] = o;
+                } else {
+                    int32_t* q1 = Ds + 4 * li;
+                    if (er != 0u && es != 0u) q1[0] = o.x;
+                    if (er != 1u && es != 1u) q1[1] = o.y;
+                    if (er != 2u && es != 2u) q1[2] = o.z;
+                    if (er != 3u && es != 3u) q1[3] = o.w;
+                }
             }
         } else {
             // disjoint entries (R10), every thread: quads g = t, t + 1024, ... (consecutive threads read
@@ -472,25 +519,16 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
         }
         // touching entries: warps 0..7, one TMEM lane (= one v) per thread
         int wa = -1, wb = -1, va = 0, vb = 0;
-        if (t < RLB_EPI) {
-            const int c = warp >> 2, v = 128 * c + 32 * (warp & 3) + lane;
-            const bool tile = 128 * c < n;
-            uint32_t R[8];
-            if (tile) {
+        if (t < RLB_EPI && mine) {
+            const int c = CL > 1 ? crank : warp >> 2;
+            const bool act = CL > 1 ? warp < 4 : 128 * c < n;
+            const int v = 128 * c + 32 * (warp & 3) + lane;
+            if (act) {
                 tc::mbar_wait(mbar, mma_phase);
                 tc::fence_after_sync();
+                uint32_t R[8];
                 tc::tmem_ld8(tmem + ((uint32_t)(32 * (warp & 3)) << 16) + 8 * c, R);
                 tc::tmem_wait_ld();
-                // Z_a = A_a.B~_b = Y_b(a) and Z_b = A_b.B~_a = Y_a(b): the new diagonal of a, b
-                if (v == sa) zz[0] = (int)R[6] + ((int)R[7] << 8);
-                if (v == sb) zz[1] = (int)R[4] + ((int)R[5] << 8);
-            }
-            group_sync(1, RLB_EPI);
-            const int Da = zz[0] + ars * brs;             // D''_a = A_a.B~_b + a_ab B~_ab
-            const int Db = zz[1] + ars * brs;
-            if (tile) {
-                if (v == sa) Dg[sa] = Da;
-                if (v == sb) Dg[sb] = Db;
                 if (v < n && v != sa && v != sb) {
                     const int xa = ((int)R[0] << 8) + (int)R[2];  // X_a = B~_v.A_a
                     const int xb = ((int)R[1] << 8) + (int)R[3];  // X_b = B~_v.A_b
@@ -499,8 +537,7 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
                     const int av = rlb_A(op1, sa, v), bv = rlb_A(op1, sb, v);
                     const int abv = rlb_B(op1, sa, v), bbv = rlb_B(op1, sb, v);
                     const int da = av - bv, db = abv - bbv;
-                    const int dv = Dg[v] - da * db;       // D''_v = D_v - dA_v dB_v
-                    Dg[v] = dv;
+                    const int dv = Dg[v];                 // D''_v (updated in the stage)
                     // R10b: δ''(a,v) and δ''(b,v) from pre-swap rows
                     wa = v > sa ? rowaddr[sa] + v : rowaddr[v] + sa;
                     va = 2 * (xa + ars * db + yb - da * brs - Da - dv + 2 * av * bbv);
@@ -512,9 +549,9 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
             mma_phase ^= 1;
         }
         __syncthreads();                                  // quads written: columns sa, sb next
-        if (wa >= 0) {
-            dwr(wa, va);
-            dwr(wb, vb);
+        if (wa >= 0) {                                    // this CTA computed them: store anywhere
+            dput(wa, va);
+            dput(wb, vb);
         }
         if (t == RLB_NT - 1) dwr(rowaddr[sa] + sb, -dw);  // swapping back restores C
         __syncthreads();

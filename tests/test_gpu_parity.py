@@ -267,13 +267,15 @@ def test_schedule_errors():
 
 @pytest.mark.parametrize("engine", RELABEL_ENGINES)
 def test_grey_density_uint16_prefix(engine):
-    """Config-4-shaped instance (uint16 B, δ≡0 plateau): first 3e5 iterations of
-    its 1e9-iteration schedule, Δ spilled to global memory."""
+    """Config-4-shaped instance (uint16 B, δ≡0 plateau): the first 1e6 iterations (3e5 on the
+    slow shared-memory engine) of its 1e9-iteration schedule, in two calls."""
     A, B = grey_density(256)
     p0 = start_perm(256, SA_SEED, 0)
     sch = O.geometric_schedule_for(A, B, p0, 10**9)
-    g, acc = _compare_run(A, B, p0, 300000, sch, mode=O.MODE_SCRATCH, opts=engine)
-    assert acc > 100000
+    I = 300000 if engine == [(RLB, 0)] else 10**6       # the shared-memory engine is slow here
+    g, acc = _compare_run(A, B, p0, I, sch, mode=O.MODE_SCRATCH, opts=engine,
+                          k_splits=[0, I // 3, I])
+    assert acc > I // 3
 
 
 def test_relabel_engine_selection():
