@@ -388,3 +388,17 @@ def test_config5_full_size_sampled_chains():
         o = O.Run(A, B, p0s[i], mode=O.MODE_SCRATCH, chain=i).run(0, cfg["iters"], sch, SA_SEED)
         assert (per[i]["cost"], per[i]["best_cost"], per[i]["accepted"], per[i]["digest"]) == (
             o["cost"], o["best_cost"], o["accepted"], o["digest"])
+
+
+def test_qaplib_fixture_through_the_abi():
+    """f4: a QAPLIB-format instance read from tests/golden goes through qap_create like any
+    other; the run is bit-exact against the oracle and reaches the brute-force optimum."""
+    import os
+    from paper_1208_2675_b200 import qaplib
+    gold = os.path.join(os.path.dirname(__file__), "golden")
+    A, B = qaplib.read_dat(os.path.join(gold, "qaplib_tiny4.dat"))
+    _, opt, _ = qaplib.read_sln(os.path.join(gold, "qaplib_tiny4.sln"))
+    p0 = start_perm(4, SA_SEED, 0)
+    I = 20000
+    g, _ = _compare_run(A, B, p0, I, O.geometric_schedule_for(A, B, p0, I))
+    assert g["best_cost"] == opt
