@@ -42,7 +42,7 @@ class _State(C.Structure):
         ("Bp", C.c_void_p), ("D", C.c_void_p),
         ("cost", C.c_int64), ("best_cost", C.c_int64),
         ("digest", C.c_uint64), ("accepted", C.c_uint64), ("near_ties", C.c_uint64),
-        ("iterations", C.c_uint64),
+        ("iterations", C.c_uint64), ("proposal", C.c_int32), ("pad", C.c_int32),
     ]
 
 
@@ -192,6 +192,7 @@ class Run:
     mode: int = MODE_DELTA
     chain: int = 0
     near_log: list = field(default_factory=list)
+    proposal: int = 0          # 0 sequential enumeration (R4), 1 random pairs (R22)
 
     def __post_init__(self):
         self.A = _i32(self.A)
@@ -203,7 +204,7 @@ class Run:
         self.Bp = np.zeros((n, n), np.int32)
         self.D = np.zeros(max(1, n * (n - 1) // 2), np.int64)
         self.st = _State()
-        self.st.n, self.st.mode = n, self.mode
+        self.st.n, self.st.mode, self.st.proposal = n, self.mode, self.proposal
         for name, arr in (("A", self.A), ("B", self.B), ("p", self.p), ("best_p", self.best_p),
                           ("Bp", self.Bp), ("D", self.D)):
             setattr(self.st, name, arr.ctypes.data)

@@ -250,6 +250,18 @@ static int check_state(const orc_state* st) {
     return 0;
 }
 
+/* R22, random proposals ("the swaps may be chosen randomly"): iteration k proposes pair
+ * index q = floor(x * M / 2^32), x the first word of Philox4x32-10(key = seed, ctr = (k lo,
+ * k hi, chain, tag 3)), i.e. (r, s) = pair(q). */
+static void random_pair(int n, int64_t M, uint64_t seed, uint64_t k, uint32_t chain, int32_t* r,
+                        int32_t* s) {
+    const uint32_t ctr[4] = {(uint32_t)k, (uint32_t)(k >> 32), chain, 3u};
+    const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    uint32_t x[4];
+    orc_philox4x32_10(ctr, key, x);
+    orc_pair(n, (int64_t)(((uint64_t)x[0] * (uint64_t)M) >> 32), r, s);
+}
+
 /* Steps (b)-(e) of P:46-50 for iterations k0 .. k0+iters-1.
  * (b) "Increment the iteration number. Retrieve the cost Δ_rs of the next
  *     possible swap (r,s)" -- sequential cyclic enumeration (R4).
@@ -271,6 +283,7 @@ int orc_sa_run(orc_state* st, uint64_t k0, uint64_t iters, int kind, double t0, 
 
     for (uint64_t it = 0; it < iters; ++it) {
         const uint64_t k = k0 + it;
+        if (st->proposal) random_pair(n, M, seed, k, chain, &r, &s);
         int64_t delta;
         if (st->mode == ORC_MODE_EQ1)
             delta = orc_delta_eq1(n, A, st->B, st->p, r, s);
@@ -318,7 +331,7 @@ int orc_sa_run(orc_state* st, uint64_t k0, uint64_t iters, int kind, double t0, 
             }
         }
         /* next possible swap: cursor + 1, cyclic (F2 / R4) */
-        if (++s == n) {
+        if (!st->proposal && ++s == n) {
             ++r;
             if (r == n - 1) r = 0;
             s = r + 1;
@@ -352,7 +365,7 @@ static void* ens_worker(void* arg) {
         int64_t c = (*j->next)++;
         pthread_mutex_unlock(j->lock);
         if (c >= j->end) break;
-        orc_state st = {n, ORC_MODE_DELTA, j->A, j->B, p, bp, Bp, D, 0, 0, 0, 0, 0, 0};
+        orc_state st = {n, ORC_MODE_DELTA, j->A, j->B, p, bp, Bp, D, 0, 0, 0, 0, 0, 0, 0, 0};
         orc_state_reset(&st, j->p0s + (size_t)(c - j->begin) * n);
         orc_sa_run(&st, 0, j->iters, j->kind, j->t0, j->tf, j->iters, j->seed,
                    j->chain_base + (uint32_t)(c - j->begin), NULL, NULL, 0, NULL, NULL, 0, 0);

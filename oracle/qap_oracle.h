@@ -72,6 +72,8 @@ typedef struct {
     int64_t* D;            /* n(n-1)/2 (DELTA mode; may be NULL otherwise) */
     int64_t cost, best_cost;
     uint64_t digest, accepted, near_ties, iterations;
+    int32_t proposal;      /* 0: sequential enumeration (R4); 1: random pairs (R22) */
+    int32_t pad;
 } orc_state;
 
 /* Set p = p0, B' = B[p0][p0], C = Eq.(1), best = C, digest = seed value,

@@ -141,3 +141,43 @@ def test_ensemble_matches_single_chains():
         assert tuple(out[i]) == (st["cost"], st["best_cost"], st["accepted"], st["near_ties"],
                                  np.int64(np.uint64(st["digest"]).view(np.int64)),
                                  st["iterations"])
+
+
+def test_random_proposals_r22():
+    """R22 (random proposals): the pair of iteration k is drawn by Philox tag 3.  Pins:
+    the three δ evaluations (Eq.(1) difference, scratch formula, maintained Δ with full
+    recomputation checks) give the same trajectory; over many iterations every pair is proposed
+    with frequency close to 1/M (within 5 sigma); a brute-force optimum is reached on a tiny
+    instance; and the sequence differs from the sequential enumeration."""
+    import itertools
+    A, B = taixxa(7, 71)
+    p0 = start_perm(7, 3, 0)
+    I = 20000
+    sch = O.geometric_schedule_for(A, B, p0, I)
+    outs = []
+    for mode in (O.MODE_EQ1, O.MODE_SCRATCH, O.MODE_DELTA):
+        r = O.Run(A, B, p0, mode=mode, proposal=1)
+        outs.append(r.run(0, I, sch, 5, check_every=1 if mode == O.MODE_DELTA else 0))
+    for key in ("cost", "best_cost", "digest", "accepted"):
+        assert outs[0][key] == outs[1][key] == outs[2][key], key
+    seq = O.Run(A, B, p0, mode=O.MODE_DELTA).run(0, I, sch, 5)
+    assert seq["digest"] != outs[2]["digest"]
+    opt = min(O.cost(A, B, np.array(q, np.int32)) for q in itertools.permutations(range(7)))
+    assert outs[2]["best_cost"] == opt
+    # frequencies: with an all-zero flow every proposal is accepted (δ = 0, R5), so the pair of
+    # iteration k is read off the permutation change of a one-iteration call
+    n6, K = 6, 6000
+    Z = np.zeros((n6, n6), np.int32)
+    Bz = taixxa(n6, 1)[1]
+    rz = O.Run(Z, Bz, np.arange(n6, dtype=np.int32), mode=O.MODE_DELTA, proposal=1)
+    sz = O.Schedule(O.COOL_GEOMETRIC, 1.0, 0.5, K)
+    counts = {}
+    for k in range(K):
+        before = rz.p.copy()
+        rz.run(k, 1, sz, 9)
+        r_, s_ = np.nonzero(before != rz.p)[0]
+        counts[(r_, s_)] = counts.get((r_, s_), 0) + 1
+    M6 = n6 * (n6 - 1) // 2
+    assert len(counts) == M6
+    exp = K / M6                                  # 400 per pair; 5 sigma = 5 * sqrt(400) = 100
+    assert all(abs(c - exp) < 100 for c in counts.values()), counts
