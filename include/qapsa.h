@@ -196,9 +196,14 @@ typedef enum {
                                     relabels, other swaps the ordinary update;
                                     2 = the same engine with the relabels off; 0 = the
                                     shared-memory kernel.  Same trajectory in every case. */
-    QAP_OPT_RELABEL_CLUSTER = 8  /* relabel engine: 8 (default) = one chain on a thread-block
+    QAP_OPT_RELABEL_CLUSTER = 8, /* relabel engine: 8 (default) = one chain on a thread-block
                                     cluster of 8 SMs, Δ spread over their shared memory (SURVEY
                                     f1); 1 = one SM, Δ in L2 */
+    QAP_OPT_PROPOSAL = 9         /* candidate order: 0 (default) = the sequential cyclic
+                                    enumeration (R4); 1 = random pairs, iteration k proposes pair
+                                    index floor(x M / 2^32), x = Philox(seed; k, chain, tag 3)
+                                    (R22); runs on the shared-memory kernel (single chain and
+                                    qap_ensemble_run) */
 } qap_option;
 qap_status qap_set_option(qap_ctx* ctx, int32_t key, int64_t value);
 /* 1 if the next qap_sa_run uses the tensor-memory engine (QAP_OPT_TENSOR_CORE), else 0. */

@@ -302,6 +302,16 @@ __device__ __forceinline__ void prepare_theta(Prep& pr, const Sched& sch, uint64
     pr.m = 2e-4f * pr.th + 2e-5f * T;
 }
 
+// Pair index proposed at iteration kk: the sequential enumeration (R4: cursor + offset) or,
+// with random proposals (R22), floor(x M / 2^32) with x = Philox(seed; kk, chain, tag 3).x
+__device__ __forceinline__ int proposal_index(bool rnd, int cur, int off, int M, uint64_t kk,
+                                              uint64_t seed, uint32_t chain) {
+    if (!rnd) return advance_cursor(cur, off, M);
+    const U4 x = philox4x32_10((uint32_t)kk, (uint32_t)(kk >> 32), chain, 3u, (uint32_t)seed,
+                               (uint32_t)(seed >> 32));
+    return (int)(((uint64_t)x.x * (uint64_t)M) >> 32);
+}
+
 // Runs iterations [k0, k_end) of one chain.  Returns the number of accepted
 // swaps (identical in every thread of the group).  QPT > 0: the thread's quads
 // are fixed at compile time (g = t - quad_lo + i * (NT - quad_lo), i < QPT).
@@ -313,7 +323,7 @@ __device__ __forceinline__ uint64_t chain_run(const TA* __restrict__ A, const Ch
                                               const Sched sch, const uint64_t seed,
                                               const uint32_t chain, const int bar_id, const int t,
                                               const int wmax, ChainScalars& io,
-                                              const NearSink sink) {
+                                              const NearSink sink, const bool rnd = false) {
     using DB = Dab<TA, TB>;
     using DT = typename DB::T;
     constexpr int NW = NT / 32;
@@ -393,7 +403,7 @@ __device__ __forceinline__ uint64_t chain_run(const TA* __restrict__ A, const Ch
 #ifdef QAPSA_PHASE_TIMERS
             if (t == 0 && !streak) atomicAdd(&g_phase_cycles[11], (unsigned long long)(clock_after((int)pre.k + Wl) - pt0));
 #endif
-            if (pre.k != kk) { PT_COUNT(8); prepare_addr(pre, n, tb.rowaddr, advance_cursor(cur, off, M), kk); }
+            if (pre.k != kk) { PT_COUNT(8); prepare_addr(pre, n, tb.rowaddr, proposal_index(rnd, cur, off, M, kk, seed, chain), kk); }
             d = cs.D[pre.addr];
             if (d <= 0) {
                 acc = true;                       // δ < 0, or δ = 0: exp(0) = 1 > r (R5)
@@ -422,7 +432,8 @@ __device__ __forceinline__ uint64_t chain_run(const TA* __restrict__ A, const Ch
         // in a run of windows without accepts, prepare the next window's addresses now
         const int Wn = min(2 * W, wmax);
         if (streak && off < Wn && (uint64_t)(Wl + off) < remaining)
-            prepare_addr(pre, n, tb.rowaddr, advance_cursor(cur, Wl + off, M), k + (uint64_t)(Wl + off));
+            prepare_addr(pre, n, tb.rowaddr, proposal_index(rnd, cur, Wl + off, M, k + (uint64_t)(Wl + off), seed, chain),
+                         k + (uint64_t)(Wl + off));
         group_sync(bar_id, NT);
         const int tv = lane < NW ? slots[lane].x : INT_MAX;
         PT_MARKD(pt1, tv);
@@ -575,7 +586,8 @@ __device__ __forceinline__ uint64_t chain_run(const TA* __restrict__ A, const Ch
             // address and threshold of this thread's candidate in the next window
             // (the window lanes are the last warps: quad warps, after their quads)
             if (off < Wnext && kacc + 1 + (uint64_t)off < k_end) {
-                prepare_addr(pre, n, tb.rowaddr, advance_cursor(cur, j + 1 + off, M),
+                prepare_addr(pre, n, tb.rowaddr,
+                             proposal_index(rnd, cur, j + 1 + off, M, kacc + 1 + (uint64_t)off, seed, chain),
                              kacc + 1 + (uint64_t)off);
                 prepare_theta(pre, sch, seed, chain);
             }

@@ -216,6 +216,7 @@ struct ChainArgs {
     unsigned long long k0, k_end, seed;
     Sched sch;
     const unsigned long long* k0_dev;   // if set, k0 is read from device memory (chained launches)
+    int proposal;            // 0 sequential enumeration (R4), 1 random pairs (R22)
 };
 
 // NFIX > 0: problem size fixed at compile time (layout offsets and loop bounds fold);
@@ -257,7 +258,7 @@ __global__ void __launch_bounds__(NT, 1) k_sa_chain(const ChainArgs a) {
     const NearSink sink{a.near_count, a.near_k, a.near_dec, a.near_cap};
     constexpr int QPT = NFIX ? quads_per_thread(NT, NFIX) : 0;
     const uint64_t acc = chain_run<TA, TB, NT, QPT>(As, cs, tb, n, ld, M, nqt, a.k0, a.k_end, a.sch,
-                                                    a.seed, 0u, 0, t, a.wmax, io, sink);
+                                                    a.seed, 0u, 0, t, a.wmax, io, sink, a.proposal != 0);
 
     for (int i = t; i < n; i += NT) {
         a.p[i] = cs.p[i];
@@ -287,6 +288,7 @@ struct EnsArgs {
     unsigned int chain_begin;
     unsigned long long iters, seed;
     Sched sch;
+    int proposal;            // 0 sequential enumeration (R4), 1 random pairs (R22)
 };
 
 template <typename TA, typename TB, int NT, int NFIX>
@@ -346,7 +348,7 @@ __global__ void __launch_bounds__(1024, 1) k_ensemble(const EnsArgs a) {
         constexpr int QPT = NFIX ? quads_per_thread(NT, NFIX) : 0;
         const uint64_t acc = chain_run<TA, TB, NT, QPT>(As, cs, tb, n, ld, M, nqt, 0ull, a.iters, a.sch,
                                                    a.seed, a.chain_begin + (unsigned)ci, bar, t,
-                                                   a.wmax, io, sink);
+                                                   a.wmax, io, sink, a.proposal != 0);
         for (int i = t; i < n; i += NT) a.best_perms[(size_t)ci * n + i] = cs.best_p[i];
         if (t == scalar_tid(NT, n)) {
             ChainResult r;

@@ -62,6 +62,7 @@ struct qap_ctx {
     // relabel engine (relabel_chain.cuh): twin classes of A, second Δ buffer for the write-back
     int use_relabel = 1;                // QAP_OPT_RELABEL
     int rlb_cluster = 8;                // QAP_OPT_RELABEL_CLUSTER: CTAs sharing Δ~ (1 = Δ~ in L2)
+    int proposal = 0;                   // QAP_OPT_PROPOSAL: 0 sequential (R4), 1 random (R22)
     int ncls = 0;
     uint8_t* dcls = nullptr;            // n
     uint16_t* dpt = nullptr;            // ncls x (n+1)
@@ -125,7 +126,9 @@ static std::vector<unsigned char> compact(int n, int ld, const int32_t* X) {
     return out;
 }
 
-static bool use_tc_engine(const qap_ctx* c) { return c->tc_ok && c->use_tc && !c->force_global; }
+static bool use_tc_engine(const qap_ctx* c) {
+    return c->tc_ok && c->use_tc && !c->force_global && c->proposal == 0;
+}
 
 static int dab_bytes(const qap_ctx* c) { return (c->ta == 1 && c->tb == 1) ? 4 : 8; }
 
@@ -188,7 +191,7 @@ static void twin_classes(int n, const int32_t* A, std::vector<uint8_t>* cls, std
 }
 
 static bool use_relabel_engine(const qap_ctx* c) {
-    return c->use_relabel && c->ta == 1 && c->tb == 2 && c->n >= 4 && c->n <= RLB_MAXN &&
+    return c->use_relabel && c->proposal == 0 && c->ta == 1 && c->tb == 2 && c->n >= 4 && c->n <= RLB_MAXN &&
            rlb_layout(c->n, c->rlb_cluster).bytes <= c->smem_optin;
 }
 
@@ -517,6 +520,7 @@ qap_status qap_sa_run(qap_ctx* c, uint64_t k0, uint64_t iters, const qap_schedul
 
     CU(cudaEventRecord(c->ev0, c->stream));
     a.k0_dev = nullptr;
+    a.proposal = c->proposal;
     if (tc) {
         a.wmax = c->wmax;
         // compile-time problem size for the BASELINE configurations, generic otherwise
@@ -741,6 +745,7 @@ qap_status qap_ensemble_run(qap_ctx* c, uint32_t chain_begin, uint32_t chain_cou
     a.A = c->dA; a.B = c->dB; a.p0s = c->ens_p0; a.res = c->ens_res; a.best_perms = c->ens_best;
     a.next_chain = c->ens_counter; a.count = (int)chain_count; a.n = n; a.ld = c->ld; a.M = c->M;
     a.rowaddr = c->drowaddr; a.qdesc = c->dqdesc; a.nqt = c->nqt;
+    a.proposal = c->proposal;
     a.wmax = std::min(c->wmax, nt); a.chain_begin = chain_begin; a.iters = iters; a.seed = seed; a.sch = sch;
     CU(cudaEventRecord(c->ev0, c->stream));
     CU(launch_ens(c, a, nt, groups, smem));
@@ -806,6 +811,10 @@ qap_status qap_set_option(qap_ctx* c, int32_t key, int64_t value) {
         case QAP_OPT_RELABEL:
             if (value < 0 || value > 2) return fail(c, QAP_E_INVALID_ARG, "relabel must be 0, 1 or 2");
             c->use_relabel = (int)value;
+            return QAP_OK;
+        case QAP_OPT_PROPOSAL:
+            if (value != 0 && value != 1) return fail(c, QAP_E_INVALID_ARG, "proposal must be 0 or 1");
+            c->proposal = (int)value;
             return QAP_OK;
         case QAP_OPT_RELABEL_CLUSTER:
             if (value != 1 && value != 8) return fail(c, QAP_E_INVALID_ARG, "relabel cluster must be 1 or 8");

@@ -36,7 +36,7 @@ def _sched(s: O.Schedule):
 
 
 def _compare_run(A, B, p0, I, sched: O.Schedule, seed=SA_SEED, opts=(), k_splits=None,
-                 mode=O.MODE_DELTA):
+                 mode=O.MODE_DELTA, proposal=0):
     """GPU run of iterations [0, I) vs the oracle; returns the GPU stats."""
     with Q.Solver(A, B, p0) as s:
         for k, v in opts:
@@ -50,7 +50,7 @@ def _compare_run(A, B, p0, I, sched: O.Schedule, seed=SA_SEED, opts=(), k_splits
         p, bp, D = s.state()
         n_near, near = s.near_ties()
         gcost = s.cost()
-    ref = O.Run(A, B, p0, mode=mode)
+    ref = O.Run(A, B, p0, mode=mode, proposal=proposal)
     o = ref.run(0, I, sched, seed, follow=near)
     assert n_near == o["near_ties"]
     assert tot_acc == o["accepted"]
@@ -402,3 +402,37 @@ def test_qaplib_fixture_through_the_abi():
     I = 20000
     g, _ = _compare_run(A, B, p0, I, O.geometric_schedule_for(A, B, p0, I))
     assert g["best_cost"] == opt
+
+
+# ---------------- f4: random proposals (R22) ----------------
+
+@pytest.mark.parametrize("n,I", [(5, 20000), (12, 100000), (50, 300000), (100, 200000)])
+def test_random_proposals_single_chain(n, I):
+    """R22 random proposals (QAP_OPT_PROPOSAL = 1) on the shared-memory engine: bit-exact
+    against the oracle's random-proposal mode, split into uneven calls."""
+    A, B = taixxa(n, 1000 + n)
+    p0 = start_perm(n, SA_SEED, 0)
+    with Q.Solver(A, B, p0) as s:
+        s.set_option(Q.QAP_OPT_PROPOSAL, 1)
+        assert s.engine() == Q.QAP_ENGINE_SHARED_MEMORY
+    _compare_run(A, B, p0, I, O.geometric_schedule_for(A, B, p0, I), opts=[(Q.QAP_OPT_PROPOSAL, 1)],
+                 k_splits=[0, 7, I // 3, I], proposal=1)
+
+
+def test_random_proposals_ensemble_chains():
+    """Random proposals in qap_ensemble_run: every chain equals the oracle's single chain with
+    the same global chain id (the proposal stream is keyed by it)."""
+    A, B = taixxa(30, 31)
+    C, I = 12, 20000
+    p0s = start_perms(30, SA_SEED, 40, C)
+    sch = O.geometric_schedule_for(A, B, p0s[0], I)
+    with Q.Solver(A, B, p0s[0]) as s:
+        s.set_option(Q.QAP_OPT_PROPOSAL, 1)
+        res = s.ensemble(40, p0s, I, _sched(sch), SA_SEED, per_chain=True)
+    for i, r in enumerate(res["per_chain"]):
+        ref = O.Run(A, B, p0s[i], chain=40 + i, proposal=1)
+        o = ref.run(0, I, sch, SA_SEED)
+        if r["near_ties"] or o["near_ties"]:
+            continue
+        assert (r["cost"], r["best_cost"], r["accepted"]) == (o["cost"], o["best_cost"], o["accepted"])
+        assert np.uint64(r["digest"]) == np.uint64(o["digest"])
