@@ -190,7 +190,8 @@ typedef enum {
                                     start of each qap_sa_run without Δ (δ from G = A B'^T, SURVEY
                                     f2) until no swap is accepted for 4096 iterations, then rebuild
                                     Δ and continue with Δ; 0 = Δ throughout.  Same trajectory. */
-    QAP_OPT_RELABEL = 7,         /* instances with 8-bit A and 16-bit B, 4 <= n <= 256 (config 4):
+    QAP_OPT_RELABEL = 7,         /* instances with 8-bit A and either 16-bit B and 4 <= n <= 256
+                                    (config 4) or 8-bit B and 128 < n <= 256:
                                     1 (default) = relabel engine: swaps of twin locations (equal
                                     rows of A off the pair, R21) are exact O(1) index
                                     relabels, other swaps the ordinary update;
