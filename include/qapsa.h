@@ -190,12 +190,14 @@ typedef enum {
                                     start of each qap_sa_run without Δ (δ from G = A B'^T, SURVEY
                                     f2) until no swap is accepted for 4096 iterations, then rebuild
                                     Δ and continue with Δ; 0 = Δ throughout.  Same trajectory. */
-    QAP_OPT_RELABEL = 7,         /* instances with 8-bit A and either 16-bit B and 4 <= n <= 256
-                                    (config 4) or 8-bit B and 128 < n <= 256:
-                                    1 (default) = relabel engine: swaps of twin locations (equal
-                                    rows of A off the pair, R21) are exact O(1) index
-                                    relabels, other swaps the ordinary update;
-                                    2 = the same engine with the relabels off; 0 = the
+    QAP_OPT_RELABEL = 7,         /* instances with 8-bit A, 4 <= n <= 256, and either 16-bit B
+                                    (config 4) or 8-bit B whose Δ would not fit the shared-memory
+                                    kernel (n = 256): 1 (default) = relabel engine: swaps of twin
+                                    locations (equal rows of A off the pair, R21) are
+                                    exact O(1) index relabels, other swaps the ordinary update
+                                    (SURVEY f3); 2 = the same engine with the relabels off; 3 =
+                                    the relabel engine for every 8-bit-A instance with
+                                    4 <= n <= 256 not on the tensor-memory engine; 0 = the
                                     shared-memory kernel.  Same trajectory in every case. */
     QAP_OPT_RELABEL_CLUSTER = 8, /* relabel engine: 8 (default) = one chain on a thread-block
                                     cluster of 8 SMs, Δ spread over their shared memory (SURVEY

@@ -190,8 +190,15 @@ static void twin_classes(int n, const int32_t* A, std::vector<uint8_t>* cls, std
     }
 }
 
+// The relabel engine runs 16-bit-B instances (config 4) and 8-bit ones whose Δ no longer fits
+// the shared-memory engine's CTA (N = 256): measured, the shared-memory engine is faster while
+// its Δ stays on chip (N = 150: 0.26 s vs 0.51 s, N = 200: 0.51 s vs 0.65 s for 1e7 iterations)
+// and slower once Δ spills to L2 (N = 256: 0.64 s vs 0.46 s).
 static bool use_relabel_engine(const qap_ctx* c) {
-    return c->use_relabel && c->proposal == 0 && c->ta == 1 && c->tb == 2 && c->n >= 4 && c->n <= RLB_MAXN &&
+    const bool spills = c->n > 128 && chain_smem_bytes(c, 1024, true) > c->smem_optin;
+    return c->use_relabel && c->proposal == 0 && c->ta == 1 && (c->tb == 2 || spills || c->use_relabel == 3) &&
+           c->n >= 4 &&
+           c->n <= RLB_MAXN &&
            rlb_layout(c->n, c->rlb_cluster).bytes <= c->smem_optin;
 }
 
@@ -550,6 +557,7 @@ qap_status qap_sa_run(qap_ctx* c, uint64_t k0, uint64_t iters, const qap_schedul
         ra.cls = c->dcls;
         ra.pt = c->dpt;
         ra.ncls = c->use_relabel == 2 ? 0 : c->ncls;
+        ra.b8 = c->tb == 1;
         ra.d_out = c->dD2;
         const int CL = c->rlb_cluster;
         auto kern = CL == 8 ? (c->n == 256 ? k_sa_relabel<256, 8> : k_sa_relabel<0, 8>)
@@ -809,7 +817,7 @@ qap_status qap_set_option(qap_ctx* c, int32_t key, int64_t value) {
             c->use_scratch = value ? 1 : 0;
             return QAP_OK;
         case QAP_OPT_RELABEL:
-            if (value < 0 || value > 2) return fail(c, QAP_E_INVALID_ARG, "relabel must be 0, 1 or 2");
+            if (value < 0 || value > 3) return fail(c, QAP_E_INVALID_ARG, "relabel must be 0, 1, 2 or 3");
             c->use_relabel = (int)value;
             return QAP_OK;
         case QAP_OPT_PROPOSAL:

@@ -1,5 +1,6 @@
 // relabel_chain.cuh -- the single-chain engine for instances with 8-bit A and 16-bit B up to
-// N = 256 (BASELINE config 4), with exact O(1) relabel swaps for twin locations
+// N = 256 (BASELINE config 4; also 8-bit B when 128 < N <= 256), with exact O(1) relabel swaps
+// for twin locations
 // (R21).
 //
 // Twins.  Locations x, y are twins when A_xz = A_yz for every z != x, y (A symmetric, zero
@@ -97,6 +98,7 @@ struct RelabelArgs {
     const uint8_t* cls;        // n: twin class of location x in [0, ncls), 0xFF = none
     const uint16_t* pt;        // ncls x (n+1): largest member of class c below x, 0xFFFF = none
     int ncls;
+    int b8;                    // B stored as 8-bit (N > 128 instances with small entries)
     int32_t* d_out;            // Δ in location space at exit (quad layout)
 };
 
@@ -176,7 +178,8 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.bar + 8);
     int32_t* D = a.D;
     const uint8_t* Ag = reinterpret_cast<const uint8_t*>(a.A);
-    const uint16_t* Bg = reinterpret_cast<const uint16_t*>(a.B);
+    const uint16_t* Bg = reinterpret_cast<const uint16_t*>(a.B);   // 16-bit B (ra.b8 == 0)
+    const uint8_t* Bg8 = reinterpret_cast<const uint8_t*>(a.B);    // 8-bit B (ra.b8 == 1)
 
     // ---- load: tables, σ = id, q = p
     for (int i = t; i < n; i += RLB_NT) {
@@ -213,7 +216,7 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
                 else {
                     const int c = kk & 255;
                     if (c < n) {
-                        const int b = Bg[q[x] * ldg + q[c]];
+                        const int b = ra.b8 ? (int)Bg8[q[x] * ldg + q[c]] : (int)Bg[q[x] * ldg + q[c]];
                         v = kk >= RLB_BL ? (b & 255) : (b >> 8);
                     }
                 }

@@ -282,7 +282,9 @@ def test_relabel_engine_selection():
     for (A, B), want in [(grey_density(256), Q.QAP_ENGINE_RELABEL),
                          (block_classes(40, [6, 3], 1), Q.QAP_ENGINE_RELABEL),
                          (block_classes(40, [6, 3], 1, hi_b=99), Q.QAP_ENGINE_TENSOR_MEMORY),
-                         (taixxa(150, 1), Q.QAP_ENGINE_SHARED_MEMORY)]:
+                         (taixxa(150, 1), Q.QAP_ENGINE_SHARED_MEMORY),    # 8-bit, Δ fits on chip
+                         (taixxa(256, 1), Q.QAP_ENGINE_RELABEL),          # 8-bit, Δ would spill
+                         (taixxa(100, 1, hi=200), Q.QAP_ENGINE_SHARED_MEMORY)]:
         n = A.shape[0]
         with Q.Solver(A, B, start_perm(n, 1, 0)) as s:
             assert s.engine() == want
@@ -436,3 +438,24 @@ def test_random_proposals_ensemble_chains():
             continue
         assert (r["cost"], r["best_cost"], r["accepted"]) == (o["cost"], o["best_cost"], o["accepted"])
         assert np.uint64(r["digest"]) == np.uint64(o["digest"])
+
+
+@pytest.mark.parametrize("engine", [pytest.param([(RLB, 3)], id="relabel"),
+                                    pytest.param([(RLB, 3), (RLBC, 1)], id="relabel_1sm"),
+                                    pytest.param([(RLB, 0)], id="smem")])
+@pytest.mark.parametrize("n", [129, 200, 256])
+def test_relabel_engine_8bit_large_n(n, engine):
+    """8-bit instances with 128 < N <= 256 (beyond the tensor-memory engine) on the relabel
+    engine (forced by QAP_OPT_RELABEL = 3 below N = 256), with and without twins, against the
+    oracle."""
+    with Q.Solver(*taixxa(n, 1), start_perm(n, 1, 0)) as s:
+        for k, v in engine:
+            s.set_option(k, v)
+        if engine[0] == (RLB, 3):
+            assert s.engine() == Q.QAP_ENGINE_RELABEL
+    A, B = taixxa(n, 500 + n)
+    p0 = start_perm(n, SA_SEED, 0)
+    I = 60000
+    _compare_run(A, B, p0, I, O.geometric_schedule_for(A, B, p0, I), opts=engine, k_splits=[0, I // 2, I])
+    A, B = block_classes(n, [40, 30], 600 + n, hi_b=255)
+    _compare_run(A, B, p0, I, O.geometric_schedule_for(A, B, p0, I), opts=engine)
