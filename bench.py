@@ -419,6 +419,9 @@ def run_ensemble(args, Q, s, pg, ws, rank, sch_t0tf):
     return {"metric": "chain-iterations/s (8192 x N=100 chains)", "unit": "chain-iterations/s",
             "value": C * I / (kms / 1e3), "value_incl_reduce": C * I / (wall_ms / 1e3),
             "kernel_ms": kms, "chains": C, "iters_per_chain": I, "n_gpus": ws,
+            "engine": ("tensor-memory: k_sa_scratch + k_delta_init + k_sa_tc over all chains, one SM per chain"
+                       if s.uses_tensor_core() else "shared-memory: k_ensemble, several chains per SM"),
+            "gpu_launches": s.last_kernel_time()[1],
             "scaling": "strong", "best_cost": res.best_cost, "best_chain": res.best_chain,
             "accepted": res.accepted, "near_ties": res.near_ties,
             "warmup": f"{args.warmup} x (<=1024 chains x 1e5 it)", "timed_runs": 1}

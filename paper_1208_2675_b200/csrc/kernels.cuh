@@ -102,6 +102,10 @@ __global__ void k_reset(const TA* __restrict__ A, const TB* __restrict__ B, cons
                         int ld, int32_t* p, int32_t* best_p, DevState* st) {
     __shared__ long long part[32];
     const int t = threadIdx.x;
+    src += (size_t)blockIdx.x * n;                // ensemble: CTA b resets chain b
+    p += (size_t)blockIdx.x * n;
+    best_p += (size_t)blockIdx.x * n;
+    st += blockIdx.x;
     long long acc = 0;
     for (int idx = t; idx < n * n; idx += blockDim.x) {
         const int i = idx / n, j = idx - i * n;
@@ -151,7 +155,9 @@ __global__ void k_cost(const TA* __restrict__ A, const TB* __restrict__ B, const
 template <typename TA, typename TB>
 __global__ void k_delta_init(const TA* __restrict__ A, const TB* __restrict__ B,
                              const int32_t* __restrict__ p, const int32_t* __restrict__ rowaddr,
-                             int n, int ld, int M, int32_t* D) {
+                             int n, int ld, int M, int32_t* D, int dstride = 0) {
+    p += (size_t)blockIdx.y * n;                  // ensemble: grid row y = chain y
+    D += (size_t)blockIdx.y * dstride;
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < M; q += gridDim.x * blockDim.x) {
         int r, s;
         tri_pair(n, q, &r, &s);
@@ -217,7 +223,35 @@ struct ChainArgs {
     Sched sch;
     const unsigned long long* k0_dev;   // if set, k0 is read from device memory (chained launches)
     int proposal;            // 0 sequential enumeration (R4), 1 random pairs (R22)
+    // ensemble launches of the tensor-memory kernels (ens = 1): CTA b runs chain chain + b on
+    // p + b n, best_p + b n, st + b, D + b dstride, k0_dev + 2 b; near ties only counted
+    int ens, dstride;
+    uint32_t chain;          // Philox chain id (R3) of the chain (of CTA 0 when ens)
 };
+
+// per-CTA chain state of a (possibly ensemble) launch of the tensor-memory kernels
+struct ChainView {
+    int32_t* p;
+    int32_t* best_p;
+    int32_t* D;
+    DevState* st;
+    const unsigned long long* k0_dev;
+    NearSink sink;
+    uint32_t chain;
+};
+__device__ __forceinline__ ChainView chain_view(const ChainArgs& a) {
+    ChainView v;
+    const int b = a.ens ? (int)blockIdx.x : 0;
+    v.p = a.p + (size_t)b * a.n;
+    v.best_p = a.best_p + (size_t)b * a.n;
+    v.D = a.D + (size_t)b * a.dstride;
+    v.st = a.st + b;
+    v.k0_dev = a.k0_dev ? a.k0_dev + 2 * b : nullptr;
+    v.sink = a.ens ? NearSink{&v.st->near_count, nullptr, nullptr, 0}
+                   : NearSink{a.near_count, a.near_k, a.near_dec, a.near_cap};
+    v.chain = a.chain + (uint32_t)b;
+    return v;
+}
 
 // NFIX > 0: problem size fixed at compile time (layout offsets and loop bounds fold);
 // NFIX == 0: any n.
@@ -361,6 +395,24 @@ __global__ void __launch_bounds__(1024, 1) k_ensemble(const EnsArgs a) {
             a.res[ci] = r;
         }
         group_sync(bar, NT);
+    }
+}
+
+// ChainResult / uint16 best permutation of every chain of a tensor-memory ensemble
+__global__ void k_ens_collect(const DevState* __restrict__ st, const int32_t* __restrict__ best_p,
+                              int count, int n, unsigned long long iters, ChainResult* res,
+                              uint16_t* best_perms) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < count * n; i += gridDim.x * blockDim.x)
+        best_perms[i] = (uint16_t)best_p[i];
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < count; c += gridDim.x * blockDim.x) {
+        ChainResult r;
+        r.cost = st[c].cost;
+        r.best_cost = st[c].best_cost;
+        r.accepted = st[c].accepted;
+        r.near_ties = st[c].near_count;
+        r.digest = st[c].digest;
+        r.iterations = iters;
+        res[c] = r;
     }
 }
 

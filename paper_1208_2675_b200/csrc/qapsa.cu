@@ -63,6 +63,11 @@ struct qap_ctx {
     int use_relabel = 1;                // QAP_OPT_RELABEL
     int rlb_cluster = 8;                // QAP_OPT_RELABEL_CLUSTER: CTAs sharing Δ~ (1 = Δ~ in L2)
     int proposal = 0;                   // QAP_OPT_PROPOSAL: 0 sequential (R4), 1 random (R22)
+    // tensor-memory ensemble (per-chain state of k_sa_scratch / k_sa_tc ensemble launches)
+    int32_t *tp = nullptr, *tbp = nullptr, *tD = nullptr;
+    DevState* tst = nullptr;
+    unsigned long long* tkout = nullptr;
+    size_t tcap = 0;
     int ncls = 0;
     uint8_t* dcls = nullptr;            // n
     uint16_t* dpt = nullptr;            // ncls x (n+1)
@@ -254,7 +259,8 @@ void qap_destroy(qap_ctx* c) {
     void* ptrs[] = {c->dA, c->dB, c->dp0, c->dp, c->dbest, c->dD, c->dperm, c->dDlin, c->drowaddr,
                     c->dqdesc, c->dst, c->dnear_count,
                     c->dnear_k, c->dnear_dec, c->dscratch, c->ens_p0, c->ens_res, c->ens_best,
-                    c->ens_counter, c->dkout, c->dcls, c->dpt, c->dD2};
+                    c->ens_counter, c->dkout, c->dcls, c->dpt, c->dD2, c->tp, c->tbp, c->tD,
+                    c->tst, c->tkout};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->ev0) cudaEventDestroy(c->ev0);
@@ -528,6 +534,9 @@ qap_status qap_sa_run(qap_ctx* c, uint64_t k0, uint64_t iters, const qap_schedul
     CU(cudaEventRecord(c->ev0, c->stream));
     a.k0_dev = nullptr;
     a.proposal = c->proposal;
+    a.ens = 0;
+    a.dstride = 0;
+    a.chain = 0u;
     if (tc) {
         a.wmax = c->wmax;
         // compile-time problem size for the BASELINE configurations, generic otherwise
@@ -714,6 +723,103 @@ static cudaError_t launch_ens(qap_ctx* c, const EnsArgs& a, int nt, int groups, 
 
 extern "C" {
 
+}  // extern "C"
+
+// Ensemble on the tensor-memory engine: one CTA (one SM: the kernels allocate all 512 TMEM
+// columns) per chain, the single-chain kernels launched over all chains at once -- the scratch
+// phase, the Δ rebuild of every chain, the Δ engine -- then the per-chain results and the argmin.
+static qap_status ensemble_tc(qap_ctx* c, uint32_t chain_begin, uint32_t chain_count, const int32_t* p0s,
+                              uint64_t iters, const Sched& sch, uint64_t seed, int64_t* best_cost,
+                              uint32_t* best_chain, int32_t* best_perm, qap_stats* sum_stats,
+                              qap_chain_result* per_chain) {
+    const int n = c->n;
+    const int dstride = c->nqt * 4 + 4;
+    CU(cudaSetDevice(c->dev));
+    if (c->ens_cap < chain_count) {
+        if (c->ens_p0) cudaFree(c->ens_p0);
+        if (c->ens_res) cudaFree(c->ens_res);
+        if (c->ens_best) cudaFree(c->ens_best);
+        c->ens_p0 = nullptr; c->ens_res = nullptr; c->ens_best = nullptr; c->ens_cap = 0;
+        if (cudaMalloc(&c->ens_p0, (size_t)chain_count * n * 4) != cudaSuccess ||
+            cudaMalloc(&c->ens_res, (size_t)chain_count * sizeof(ChainResult)) != cudaSuccess ||
+            cudaMalloc(&c->ens_best, (size_t)chain_count * n * 2) != cudaSuccess)
+            return fail(c, QAP_E_NOMEM, "ensemble buffers");
+        c->ens_cap = chain_count;
+    }
+    if (c->tcap < chain_count) {
+        void* ptrs[] = {c->tp, c->tbp, c->tD, c->tst, c->tkout};
+        for (void* q : ptrs)
+            if (q) cudaFree(q);
+        c->tp = c->tbp = c->tD = nullptr; c->tst = nullptr; c->tkout = nullptr; c->tcap = 0;
+        if (cudaMalloc(&c->tp, (size_t)chain_count * n * 4) != cudaSuccess ||
+            cudaMalloc(&c->tbp, (size_t)chain_count * n * 4) != cudaSuccess ||
+            cudaMalloc(&c->tD, (size_t)chain_count * dstride * 4) != cudaSuccess ||
+            cudaMalloc(&c->tst, (size_t)chain_count * sizeof(DevState)) != cudaSuccess ||
+            cudaMalloc(&c->tkout, (size_t)chain_count * 2 * sizeof(unsigned long long)) != cudaSuccess)
+            return fail(c, QAP_E_NOMEM, "tensor-memory ensemble buffers");
+        c->tcap = chain_count;
+    }
+    CU(cudaMemcpyAsync(c->ens_p0, p0s, (size_t)chain_count * n * 4, cudaMemcpyHostToDevice, c->stream));
+    ChainArgs a;
+    a.A = c->dA; a.B = c->dB; a.p = c->tp; a.best_p = c->tbp; a.D = c->tD; a.st = c->tst;
+    a.rowaddr = c->drowaddr; a.qdesc = c->dqdesc; a.nqt = c->nqt;
+    a.near_count = nullptr; a.near_k = nullptr; a.near_dec = nullptr; a.near_cap = 0;
+    a.n = n; a.ld = c->ld; a.M = c->M; a.wmax = c->wmax;
+    a.k0 = 0; a.k_end = iters; a.seed = seed; a.sch = sch;
+    a.k0_dev = nullptr; a.proposal = 0;
+    a.ens = 1; a.dstride = dstride; a.chain = chain_begin;
+    CU(cudaEventRecord(c->ev0, c->stream));
+    k_reset<uint8_t, uint8_t><<<chain_count, 512, 0, c->stream>>>((const uint8_t*)c->dA, (const uint8_t*)c->dB,
+                                                                   c->ens_p0, n, c->ld, c->tp, c->tbp, c->tst);
+    CU(cudaGetLastError());
+    auto ks = n == 100 ? k_sa_scratch<100> : n == 50 ? k_sa_scratch<50> : n == 12 ? k_sa_scratch<12> : k_sa_scratch<0>;
+    // at least half of the shared memory, so that one chain's CTA holds an SM (and its TMEM) alone
+    const int ssm = std::max(sc_layout(c->ld).bytes, c->smem_optin / 2 + 1024);
+    CU(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, ssm));
+    ks<<<chain_count, TCS_NT, ssm, c->stream>>>(a, c->tkout);
+    CU(cudaGetLastError());
+    const int dt = 256, db = (c->M + dt - 1) / dt;
+    k_delta_init<uint8_t, uint8_t><<<dim3(db, chain_count), dt, 0, c->stream>>>(
+        (const uint8_t*)c->dA, (const uint8_t*)c->dB, c->tp, c->drowaddr, n, c->ld, c->M, c->tD, dstride);
+    CU(cudaGetLastError());
+    a.k0_dev = c->tkout;
+    auto kern = n == 100 ? k_sa_tc<100> : n == 50 ? k_sa_tc<50> : n == 12 ? k_sa_tc<12> : k_sa_tc<0>;
+    const int tsm = tc_layout(c->ld).bytes;
+    CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm));
+    kern<<<chain_count, TCK_NT, tsm, c->stream>>>(a);
+    CU(cudaGetLastError());
+    CU(cudaEventRecord(c->ev1, c->stream));
+    k_ens_collect<<<std::min<int>(1024, (chain_count * n + 255) / 256), 256, 0, c->stream>>>(
+        c->tst, c->tbp, (int)chain_count, n, iters, c->ens_res, c->ens_best);
+    CU(cudaGetLastError());
+    k_ens_reduce<<<1, 1024, 0, c->stream>>>(c->ens_res, (int)chain_count, c->dscratch);
+    CU(cudaGetLastError());
+    long long red[8];
+    CU(cudaMemcpyAsync(red, c->dscratch, sizeof red, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    const int bi = (int)red[1];
+    std::vector<uint16_t> bp(n);
+    CU(cudaMemcpy(bp.data(), c->ens_best + (size_t)bi * n, n * 2, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < n; ++i) best_perm[i] = bp[i];
+    *best_cost = red[0];
+    *best_chain = chain_begin + (uint32_t)bi;
+    if (sum_stats) {
+        sum_stats->iterations = iters * (uint64_t)chain_count;
+        sum_stats->accepted = (uint64_t)red[2];
+        sum_stats->near_ties = (uint64_t)red[3];
+        sum_stats->digest = (uint64_t)red[4];
+        sum_stats->cost = red[5];
+        sum_stats->best_cost = red[0];
+    }
+    if (per_chain)
+        CU(cudaMemcpy(per_chain, c->ens_res, (size_t)chain_count * sizeof(ChainResult), cudaMemcpyDeviceToHost));
+    CU(cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1));
+    c->last_launches = 4;
+    return QAP_OK;
+}
+
+extern "C" {
+
 qap_status qap_ensemble_run(qap_ctx* c, uint32_t chain_begin, uint32_t chain_count, const int32_t* p0s,
                             uint64_t iters, const qap_schedule* s, uint64_t seed, int64_t* best_cost,
                             uint32_t* best_chain, int32_t* best_perm, qap_stats* sum_stats,
@@ -727,6 +833,9 @@ qap_status qap_ensemble_run(qap_ctx* c, uint32_t chain_begin, uint32_t chain_cou
     const int n = c->n;
     for (uint32_t i = 0; i < chain_count; ++i)
         if (!is_perm(n, p0s + (size_t)i * n)) return fail(c, QAP_E_DIMENSION, "a start permutation is invalid");
+    if (use_tc_engine(c))
+        return ensemble_tc(c, chain_begin, chain_count, p0s, iters, sch, seed, best_cost, best_chain,
+                           best_perm, sum_stats, per_chain);
     const int nt = (c->ta == 1 && c->tb == 1) ? c->ens_group : 128;
     const GroupLayout L = group_layout(n, c->ld, c->nqt, c->tb, nt / 32, true, dab_bytes(c));
     const int a_bytes = cta_prefix_bytes(n, c->ld, c->ta, c->nqt);

@@ -61,6 +61,7 @@ __host__ __device__ inline ScLayout sc_layout(int ld) {
 template <int NFIX>
 __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, unsigned long long* k_out) {
     extern __shared__ __align__(16) unsigned char smem[];
+    const ChainView cv = chain_view(a);          // this CTA's chain (ensemble launches)
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int n = NFIX ? NFIX : a.n;
     const int ld = NFIX ? row_stride(NFIX, true) : a.ld;
@@ -88,8 +89,8 @@ __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, uns
     copy_words(As, a.A, n * ld, t, TCS_NT);
     copy_words(Bs, a.B, n * ld, t, TCS_NT);
     for (int i = t; i < n; i += TCS_NT) {
-        p[i] = (uint16_t)a.p[i];
-        best_p[i] = (uint16_t)a.best_p[i];
+        p[i] = (uint16_t)cv.p[i];
+        best_p[i] = (uint16_t)cv.best_p[i];
     }
     for (int i = t; i < 256 * 32 / 16; i += TCS_NT) reinterpret_cast<uint4*>(Rg)[i] = make_uint4(0, 0, 0, 0);
     if (warp == 0) tc::tmem_alloc(tmem_slot, TCS_COLS);
@@ -143,9 +144,9 @@ __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, uns
 
     const Sched sch = a.sch;
     const uint64_t seed = a.seed, k_end = a.k_end;
-    const NearSink sink{a.near_count, a.near_k, a.near_dec, a.near_cap};
-    int64_t cost = a.st->cost, best = a.st->best_cost;
-    uint64_t digest = a.st->digest;
+    const NearSink sink = cv.sink;
+    int64_t cost = cv.st->cost, best = cv.st->best_cost;
+    uint64_t digest = cv.st->digest;
     uint64_t k = a.k0, accepted = 0, k_last = a.k0;
     int u0, v0;
     tri_pair(n, (int)(k % (uint64_t)M), &u0, &v0);
@@ -221,11 +222,11 @@ __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, uns
                     const int o = rb[i] + v;
                     float th, m;
                     if (o < pnk) { const float2 q = thm[o]; th = q.x; m = q.y; }
-                    else theta_of(sch, seed, k + (uint64_t)o, &th, &m);
+                    else theta_of(sch, seed, cv.chain, k + (uint64_t)o, &th, &m);
                     const float df = (float)dd[i];
                     bool ac = df < th - m;
                     if (!ac && !(df > th + m)) {  // inside the margin: exact double test (R16)
-                        const int x = tc_exact(dd[i], k + (uint64_t)o, sch, seed);
+                        const int x = tc_exact(dd[i], k + (uint64_t)o, sch, seed, cv.chain);
                         ac = x & 1;
                         near_mask |= (unsigned)((x >> 1) & 1) << i;
                     }
@@ -361,7 +362,7 @@ __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, uns
         const uint64_t kacc = (uint64_t)(uint32_t)rec[2] | ((uint64_t)(uint32_t)rec[3] << 32);
         for (int o = v; o < npn; o += 128) {
             float th, m;
-            theta_of(sch, seed, kacc + 1 + (uint64_t)o, &th, &m);
+            theta_of(sch, seed, cv.chain, kacc + 1 + (uint64_t)o, &th, &m);
             thm[o] = make_float2(th, m);
         }
         __syncwarp();
@@ -378,17 +379,18 @@ __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, uns
 #endif
     __syncthreads();
     for (int i = t; i < n; i += TCS_NT) {
-        a.p[i] = p[i];
-        a.best_p[i] = best_p[i];
+        cv.p[i] = p[i];
+        cv.best_p[i] = best_p[i];
     }
     if (t == 0) {
-        a.st->cost = cost;
-        a.st->best_cost = best;
-        a.st->accepted += accepted;
-        k_out[0] = k;                            // iteration reached (the Δ engine starts here)
-        k_out[1] = accepted;                     // swaps accepted in this phase
+        cv.st->cost = cost;
+        cv.st->best_cost = best;
+        cv.st->accepted += accepted;
+        unsigned long long* ko = k_out + (a.ens ? 2 * blockIdx.x : 0);
+        ko[0] = k;                               // iteration reached (the Δ engine starts here)
+        ko[1] = accepted;                        // swaps accepted in this phase
     }
-    if (t == 128) a.st->digest = digest;
+    if (t == 128) cv.st->digest = digest;
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();

@@ -156,24 +156,26 @@ __device__ __forceinline__ int rej_bound(const Sched& sch, uint64_t k) {
 }
 
 // θ = -T_k ln r_k in float and its margin (chain.cuh prepare_theta)
-__device__ __forceinline__ void theta_of(const Sched& sch, uint64_t seed, uint64_t kk, float* th, float* m) {
+__device__ __forceinline__ void theta_of(const Sched& sch, uint64_t seed, uint32_t chain, uint64_t kk,
+                                         float* th, float* m) {
     Prep pr;
     pr.k = kk;
-    prepare_theta(pr, sch, seed, 0u);
+    prepare_theta(pr, sch, seed, chain);
     *th = pr.th;
     *m = pr.m;
 }
 // exact double-precision Eq.(2) inside the float margin (rare; kept out of line):
 // bit 0 = accept, bit 1 = near tie (R16)
-__device__ __noinline__ int tc_exact(int d, uint64_t kk, Sched sch, uint64_t seed) {
+__device__ __noinline__ int tc_exact(int d, uint64_t kk, Sched sch, uint64_t seed, uint32_t chain) {
     bool near = false;
-    const bool acc = metropolis(d, temperature(sch, kk), uniform_r(seed, kk, 0u), &near);
+    const bool acc = metropolis(d, temperature(sch, kk), uniform_r(seed, kk, chain), &near);
     return (acc ? 1 : 0) | (near ? 2 : 0);
 }
 
 template <int NFIX>
 __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
+    const ChainView cv = chain_view(a);          // this CTA's chain (ensemble launches)
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int n = NFIX ? NFIX : a.n;
     const int ld = NFIX ? row_stride(NFIX, true) : a.ld;
@@ -203,8 +205,8 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
     copy_words(As, a.A, n * ld, t, TCK_NT);
     copy_words(Bs, a.B, n * ld, t, TCK_NT);
     for (int i = t; i < n; i += TCK_NT) {
-        p[i] = (uint16_t)a.p[i];
-        best_p[i] = (uint16_t)a.best_p[i];
+        p[i] = (uint16_t)cv.p[i];
+        best_p[i] = (uint16_t)cv.best_p[i];
     }
     for (int i = t; i < 3 * 128 * 32 / 16; i += TCK_NT)    // Rd, Rg := 0
         reinterpret_cast<uint4*>(Rd)[i] = make_uint4(0, 0, 0, 0);
@@ -243,7 +245,7 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
 #pragma unroll
             for (int jj = 0; jj < 32; ++jj) {
                 const int u = 32 * c + jj;
-                vals[jj] = (u < v && v < n) ? (uint32_t)a.D[a.rowaddr[u] + v] : 0u;
+                vals[jj] = (u < v && v < n) ? (uint32_t)cv.D[a.rowaddr[u] + v] : 0u;
             }
             tc::tmem_st32(tm + quad_lane + 32 * c, vals);
         }
@@ -268,10 +270,10 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
 
     const Sched sch = a.sch;
     const uint64_t seed = a.seed, k_end = a.k_end;
-    const NearSink sink{a.near_count, a.near_k, a.near_dec, a.near_cap};
-    int64_t cost = a.st->cost, best = a.st->best_cost;
-    uint64_t digest = a.st->digest;
-    uint64_t k = a.k0_dev ? *a.k0_dev : a.k0, accepted = 0;
+    const NearSink sink = cv.sink;
+    int64_t cost = cv.st->cost, best = cv.st->best_cost;
+    uint64_t digest = cv.st->digest;
+    uint64_t k = cv.k0_dev ? *cv.k0_dev : a.k0, accepted = 0;
     int u0, v0;
     tri_pair(n, (int)(k % (uint64_t)M), &u0, &v0);
     const int wmax = a.wmax;
@@ -354,11 +356,11 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
                         const int d = (int)dd[i];
                         float th, m;
                         if (o < pnk) { const float2 q = thm[o]; th = q.x; m = q.y; }
-                        else theta_of(sch, seed, k + (uint64_t)o, &th, &m);
+                        else theta_of(sch, seed, cv.chain, k + (uint64_t)o, &th, &m);
                         const float df = (float)d;
                         bool ac = df < th - m;
                         if (!ac && !(df > th + m)) {  // inside the margin: exact double test (R16)
-                            const int x = tc_exact(d, k + (uint64_t)o, sch, seed);
+                            const int x = tc_exact(d, k + (uint64_t)o, sch, seed, cv.chain);
                             ac = x & 1;
                             near_mask |= (unsigned)((x >> 1) & 1) << (4 * g + i);
                         }
@@ -508,7 +510,7 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
             if (kacc + 1 + (uint64_t)Wln > k_end) Wln = (int)(k_end - kacc - 1);
             for (int o = v; o < Wln && o < TCK_TH; o += 128) {
                 float th, m;
-                theta_of(sch, seed, kacc + 1 + (uint64_t)o, &th, &m);
+                theta_of(sch, seed, cv.chain, kacc + 1 + (uint64_t)o, &th, &m);
                 thm[o] = make_float2(th, m);
             }
             if (t == 128) digest = digest_step(digest, kacc, r, s);
@@ -591,8 +593,8 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
 #endif
     __syncthreads();
     for (int i = t; i < n; i += TCK_NT) {
-        a.p[i] = p[i];
-        a.best_p[i] = best_p[i];
+        cv.p[i] = p[i];
+        cv.best_p[i] = best_p[i];
     }
     if (lanew) {
 #pragma unroll 1
@@ -603,15 +605,15 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
 #pragma unroll
             for (int jj = 0; jj < 32; ++jj) {
                 const int u = 32 * c + jj;
-                if (u < v && v < n) a.D[a.rowaddr[u] + v] = (int32_t)vals[jj];
+                if (u < v && v < n) cv.D[a.rowaddr[u] + v] = (int32_t)vals[jj];
             }
         }
     }
     if (t == 128) {                              // helper 0 holds the digest
-        a.st->cost = cost;
-        a.st->best_cost = best;
-        a.st->digest = digest;
-        a.st->accepted += accepted;
+        cv.st->cost = cost;
+        cv.st->best_cost = best;
+        cv.st->digest = digest;
+        cv.st->accepted += accepted;
     }
     tc::fence_before_sync();
     __syncthreads();

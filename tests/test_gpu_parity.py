@@ -459,3 +459,27 @@ def test_relabel_engine_8bit_large_n(n, engine):
     _compare_run(A, B, p0, I, O.geometric_schedule_for(A, B, p0, I), opts=engine, k_splits=[0, I // 2, I])
     A, B = block_classes(n, [40, 30], 600 + n, hi_b=255)
     _compare_run(A, B, p0, I, O.geometric_schedule_for(A, B, p0, I), opts=engine)
+
+
+def test_ensemble_tensor_memory_vs_shared_memory():
+    """qap_ensemble_run on the tensor-memory engine (default where eligible: one SM per chain,
+    scratch phase, Δ rebuild, Δ engine) and on the shared-memory kernel give the same result
+    for every chain, and both match the oracle's single chains."""
+    A, B = taixxa(60, 61)
+    C, I = 40, 50000
+    p0s = start_perms(60, SA_SEED, 7, C)
+    sch = O.geometric_schedule_for(A, B, p0s[0], I)
+    out = {}
+    for tcv in (1, 0):
+        with Q.Solver(A, B, p0s[0]) as s:
+            s.set_option(TC, tcv)
+            out[tcv] = s.ensemble(7, p0s, I, _sched(sch), SA_SEED, per_chain=True)
+    assert out[1]["best_cost"] == out[0]["best_cost"] and out[1]["best_chain"] == out[0]["best_chain"]
+    np.testing.assert_array_equal(out[1]["best_perm"], out[0]["best_perm"])
+    for i, (r1, r0) in enumerate(zip(out[1]["per_chain"], out[0]["per_chain"])):
+        assert r1 == r0, i
+        if i < 6:
+            o = O.Run(A, B, p0s[i], chain=7 + i).run(0, I, sch, SA_SEED)
+            if not o["near_ties"]:
+                assert (r1["cost"], r1["best_cost"], r1["accepted"]) == (o["cost"], o["best_cost"], o["accepted"])
+                assert np.uint64(r1["digest"]) == np.uint64(o["digest"])
