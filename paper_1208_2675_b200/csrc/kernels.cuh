@@ -239,16 +239,24 @@ struct ChainView {
     NearSink sink;
     uint32_t chain;
 };
+// ENS = false (single-chain launches): the chain id is the constant 0, so the Philox rounds of
+// the thresholds fold it as before
+template <bool ENS>
 __device__ __forceinline__ ChainView chain_view(const ChainArgs& a) {
     ChainView v;
-    const int b = a.ens ? (int)blockIdx.x : 0;
+    if (!ENS) {
+        v.p = a.p; v.best_p = a.best_p; v.D = a.D; v.st = a.st; v.k0_dev = a.k0_dev;
+        v.sink = NearSink{a.near_count, a.near_k, a.near_dec, a.near_cap};
+        v.chain = 0u;
+        return v;
+    }
+    const int b = (int)blockIdx.x;
     v.p = a.p + (size_t)b * a.n;
     v.best_p = a.best_p + (size_t)b * a.n;
     v.D = a.D + (size_t)b * a.dstride;
     v.st = a.st + b;
     v.k0_dev = a.k0_dev ? a.k0_dev + 2 * b : nullptr;
-    v.sink = a.ens ? NearSink{&v.st->near_count, nullptr, nullptr, 0}
-                   : NearSink{a.near_count, a.near_k, a.near_dec, a.near_cap};
+    v.sink = NearSink{&v.st->near_count, nullptr, nullptr, 0};
     v.chain = a.chain + (uint32_t)b;
     return v;
 }

@@ -772,7 +772,8 @@ static qap_status ensemble_tc(qap_ctx* c, uint32_t chain_begin, uint32_t chain_c
     k_reset<uint8_t, uint8_t><<<chain_count, 512, 0, c->stream>>>((const uint8_t*)c->dA, (const uint8_t*)c->dB,
                                                                    c->ens_p0, n, c->ld, c->tp, c->tbp, c->tst);
     CU(cudaGetLastError());
-    auto ks = n == 100 ? k_sa_scratch<100> : n == 50 ? k_sa_scratch<50> : n == 12 ? k_sa_scratch<12> : k_sa_scratch<0>;
+    auto ks = n == 100 ? k_sa_scratch<100, true> : n == 50 ? k_sa_scratch<50, true>
+            : n == 12 ? k_sa_scratch<12, true> : k_sa_scratch<0, true>;
     // at least half of the shared memory, so that one chain's CTA holds an SM (and its TMEM) alone
     const int ssm = std::max(sc_layout(c->ld).bytes, c->smem_optin / 2 + 1024);
     CU(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, ssm));
@@ -783,7 +784,8 @@ static qap_status ensemble_tc(qap_ctx* c, uint32_t chain_begin, uint32_t chain_c
         (const uint8_t*)c->dA, (const uint8_t*)c->dB, c->tp, c->drowaddr, n, c->ld, c->M, c->tD, dstride);
     CU(cudaGetLastError());
     a.k0_dev = c->tkout;
-    auto kern = n == 100 ? k_sa_tc<100> : n == 50 ? k_sa_tc<50> : n == 12 ? k_sa_tc<12> : k_sa_tc<0>;
+    auto kern = n == 100 ? k_sa_tc<100, true> : n == 50 ? k_sa_tc<50, true> : n == 12 ? k_sa_tc<12, true>
+              : k_sa_tc<0, true>;
     const int tsm = tc_layout(c->ld).bytes;
     CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm));
     kern<<<chain_count, TCK_NT, tsm, c->stream>>>(a);

@@ -58,10 +58,10 @@ __host__ __device__ inline ScLayout sc_layout(int ld) {
     return L;
 }
 
-template <int NFIX>
+template <int NFIX, bool ENS = false>
 __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, unsigned long long* k_out) {
     extern __shared__ __align__(16) unsigned char smem[];
-    const ChainView cv = chain_view(a);          // this CTA's chain (ensemble launches)
+    const ChainView cv = chain_view<ENS>(a);     // this CTA's chain (ensemble launches)
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int n = NFIX ? NFIX : a.n;
     const int ld = NFIX ? row_stride(NFIX, true) : a.ld;
@@ -386,7 +386,7 @@ __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, uns
         cv.st->cost = cost;
         cv.st->best_cost = best;
         cv.st->accepted += accepted;
-        unsigned long long* ko = k_out + (a.ens ? 2 * blockIdx.x : 0);
+        unsigned long long* ko = k_out + (ENS ? 2 * blockIdx.x : 0);
         ko[0] = k;                               // iteration reached (the Δ engine starts here)
         ko[1] = accepted;                        // swaps accepted in this phase
     }

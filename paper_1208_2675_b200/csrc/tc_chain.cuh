@@ -172,10 +172,10 @@ __device__ __noinline__ int tc_exact(int d, uint64_t kk, Sched sch, uint64_t see
     return (acc ? 1 : 0) | (near ? 2 : 0);
 }
 
-template <int NFIX>
+template <int NFIX, bool ENS = false>
 __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
-    const ChainView cv = chain_view(a);          // this CTA's chain (ensemble launches)
+    const ChainView cv = chain_view<ENS>(a);     // this CTA's chain (ensemble launches)
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int n = NFIX ? NFIX : a.n;
     const int ld = NFIX ? row_stride(NFIX, true) : a.ld;
