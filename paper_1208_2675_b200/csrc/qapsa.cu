@@ -774,8 +774,9 @@ static qap_status ensemble_tc(qap_ctx* c, uint32_t chain_begin, uint32_t chain_c
     CU(cudaGetLastError());
     auto ks = n == 100 ? k_sa_scratch<100, true> : n == 50 ? k_sa_scratch<50, true>
             : n == 12 ? k_sa_scratch<12, true> : k_sa_scratch<0, true>;
-    // at least half of the shared memory, so that one chain's CTA holds an SM (and its TMEM) alone
-    const int ssm = std::max(sc_layout(c->ld).bytes, c->smem_optin / 2 + 1024);
+    // more than a third of the shared memory: at most two chains' CTAs per SM, whose 2 x 256 TMEM
+    // columns fill the SM's 512
+    const int ssm = std::max(sc_layout(c->ld).bytes, c->smem_optin / 3 + 1024);
     CU(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, ssm));
     ks<<<chain_count, TCS_NT, ssm, c->stream>>>(a, c->tkout);
     CU(cudaGetLastError());

@@ -31,12 +31,14 @@ namespace qapsa {
 constexpr int TCS_NT = 256;
 constexpr uint32_t TCS_COL_G = 0;        // G: TMEM columns [0, 128)
 constexpr uint32_t TCS_COL_H = 128;      // H: TMEM columns [128, 256)
-constexpr uint32_t TCS_COL_L = 256;      // A operand of the update: [dA, -dBf] (K = 32)
-constexpr uint32_t TCS_COLS = 512;
+constexpr uint32_t TCS_COL_L = 256;      // single chain: A operand of the update [dA, -dBf] (K = 32)
+// TMEM columns: a single chain keeps the update's A operand in TMEM (512 columns); an ensemble
+// launch keeps it in shared memory so that G and H (256 columns) let two chains share an SM
+template <bool ENS> __host__ __device__ constexpr uint32_t tcs_cols() { return ENS ? 256u : 512u; }
 constexpr uint64_t TCS_SWITCH_GAP = 4096;   // switch to the Δ engine after this many iterations without an accept
 
 struct ScLayout {
-    int a, b, rg, tmp, p, bestp, dg, xch, slots, rec, thm, misc, bytes;
+    int a, b, rg, la, tmp, p, bestp, dg, xch, slots, rec, thm, misc, bytes;
 };
 __host__ __device__ inline ScLayout sc_layout(int ld) {
     ScLayout L;
@@ -45,6 +47,7 @@ __host__ __device__ inline ScLayout sc_layout(int ld) {
     L.b = o;     o += 128 * ld;
     o = (o + 1023) & ~1023;
     L.rg = o;    o += 256 * 32;                 // [G | H] update B operand, K-major canonical (SBO 256)
+    L.la = o;    o += 128 * 32;                 // its A operand [dA, -dBf], same layout
     L.tmp = o;   o += 2 * 128 * 128;            // init only: A, C canonical (SBO 1024)
     L.p = o;     o += 128 * 2;
     L.bestp = o; o += 128 * 2;
@@ -70,6 +73,7 @@ __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, uns
     uint8_t* As = smem + L.a;
     uint8_t* Bs = smem + L.b;
     uint8_t* Rg = smem + L.rg;
+    uint8_t* La = smem + L.la;
     uint16_t* p = reinterpret_cast<uint16_t*>(smem + L.p);
     uint16_t* best_p = reinterpret_cast<uint16_t*>(smem + L.bestp);
     int* Dg = reinterpret_cast<int*>(smem + L.dg);
@@ -92,13 +96,18 @@ __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, uns
         p[i] = (uint16_t)cv.p[i];
         best_p[i] = (uint16_t)cv.best_p[i];
     }
-    for (int i = t; i < 256 * 32 / 16; i += TCS_NT) reinterpret_cast<uint4*>(Rg)[i] = make_uint4(0, 0, 0, 0);
-    if (warp == 0) tc::tmem_alloc(tmem_slot, TCS_COLS);
+    for (int i = t; i < (256 + 128) * 32 / 16; i += TCS_NT) reinterpret_cast<uint4*>(Rg)[i] = make_uint4(0, 0, 0, 0);
+    if (warp == 0) tc::tmem_alloc(tmem_slot, tcs_cols<ENS>());
     if (t == 0) { tc::mbar_init(mbar, 1); tc::mbar_init(mbar_t, 4); }
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
     const uint32_t tm = *tmem_slot;
+    if (!ENS && lanew) {
+        tc::tmem_st4(tm + quad_lane + TCS_COL_L, 0u, 0u, 0u, 0u);
+        tc::tmem_st4(tm + quad_lane + TCS_COL_L + 4, 0u, 0u, 0u, 0u);
+        tc::tmem_wait_st();
+    }
     {
         uint8_t* Ac = smem + L.tmp;
         uint8_t* Cc = Ac + 128 * 128;
@@ -107,11 +116,6 @@ __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, uns
             const bool in = x < n && kk < n;
             Ac[cofs(x, kk)] = in ? As[x * ld + kk] : (uint8_t)0;
             Cc[cofs(x, kk)] = in ? Bs[x * ld + p[kk]] : (uint8_t)0;
-        }
-        if (lanew) {
-            tc::tmem_st4(tm + quad_lane + TCS_COL_L, 0u, 0u, 0u, 0u);
-            tc::tmem_st4(tm + quad_lane + TCS_COL_L + 4, 0u, 0u, 0u, 0u);
-            tc::tmem_wait_st();
         }
         tc::fence_proxy_async();
         tc::fence_before_sync();
@@ -291,8 +295,9 @@ __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, uns
         uint32_t gps, gpr;                       // G[v][p(s)], G[v][p(r)] (pre-update)
         tc::tmem_ld1(tm + quad_lane + TCS_COL_G + (uint32_t)ps, gps);
         tc::tmem_ld1(tm + quad_lane + TCS_COL_G + (uint32_t)pr, gpr);
-        tc::tmem_st1(tm + quad_lane + TCS_COL_L, b8(dA) | (b8(-dBf) << 8));
         const int ro = (v >> 3) * 256 + (v & 7) * 16;
+        if (ENS) *reinterpret_cast<uint16_t*>(La + ro) = (uint16_t)(b8(dA) | (b8(-dBf) << 8));   // A row v
+        else tc::tmem_st1(tm + quad_lane + TCS_COL_L, b8(dA) | (b8(-dBf) << 8));
         *reinterpret_cast<uint32_t*>(Rg + ro) = b8(-dBf);               // G rows: facility v
         *reinterpret_cast<uint32_t*>(Rg + 4096 + ro) = b8(dA) << 8;    // H rows: location v
         const int ars = As[r * ld + s], brs = Bs[pr * ld + ps];
@@ -319,7 +324,11 @@ __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, uns
         if (t == 0) {
             tc::fence_after_sync();
             // [G | H] (256 columns) += [dA, -dBf] [[-dBf, 0]; [0, dA]]^T
-            tc::mma_i8_ts(tm + TCS_COL_G, tm + TCS_COL_L, tc::smem_desc(tc::smem_u32(Rg), 128, 256), id_gh, true);
+            if (ENS)
+                tc::mma_i8(tm + TCS_COL_G, tc::smem_desc(tc::smem_u32(La), 128, 256),
+                           tc::smem_desc(tc::smem_u32(Rg), 128, 256), id_gh, true);
+            else
+                tc::mma_i8_ts(tm + TCS_COL_G, tm + TCS_COL_L, tc::smem_desc(tc::smem_u32(Rg), 128, 256), id_gh, true);
             tc::mma_commit(mbar);
         }
         if (vin) Dg[v] = dnew;
@@ -394,7 +403,7 @@ __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, uns
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
-    if (warp == 0) tc::tmem_dealloc(tm, TCS_COLS);
+    if (warp == 0) tc::tmem_dealloc(tm, tcs_cols<ENS>());
 }
 
 }  // namespace qapsa
