@@ -227,6 +227,8 @@ struct ChainArgs {
     // p + b n, best_p + b n, st + b, D + b dstride, k0_dev + 2 b; near ties only counted
     int ens, dstride;
     uint32_t chain;          // Philox chain id (R3) of the chain (of CTA 0 when ens)
+    unsigned long long switch_gap;   // scratch phase: switch to Δ after this many iterations
+                                     // without an accept (0 = TCS_SWITCH_GAP)
 };
 
 // per-CTA chain state of a (possibly ensemble) launch of the tensor-memory kernels

@@ -167,7 +167,8 @@ __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, uns
 
   if (lanew) {
     uint32_t ph_t = 0;                           // phase of the thresholds mbarrier (one per accept)
-    while (k < k_end && k - k_last < TCS_SWITCH_GAP) {
+    const uint64_t gap = a.switch_gap ? a.switch_gap : TCS_SWITCH_GAP;
+    while (k < k_end && k - k_last < gap) {
         // ---------------- window: rows u0 .. u0+R-1 (R <= 4) ----------------
         TCT_MARK(pt0, u0 + v0);
         const int R = win_rows<4>(n, u0), L0 = n - v0, m1 = n - 1 - u0;
