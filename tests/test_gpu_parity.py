@@ -297,7 +297,8 @@ def test_relabel_engine_selection():
                                                 (33, [8, 5, 3], 3, 50000),
                                                 (64, [20, 10, 6, 3], 4, 100000),
                                                 (130, [40, 30, 2], 5, 60000),
-                                                (256, [92, 100, 3], 6, 60000)])
+                                                (256, [92, 100, 3], 6, 60000),
+                                                (90, [9, 8, 7, 6, 5, 4], 7, 60000)])   # > RLB_MAXCLS classes
 @pytest.mark.parametrize("engine", RELABEL_ENGINES[:3])
 def test_relabel_engine_twin_classes(n, sizes, seed, iters, engine):
     """Instances with twin classes (R21) and 16-bit B: Δ, p, best_p, C, digest and every
