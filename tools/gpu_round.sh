@@ -24,3 +24,12 @@ timeout 120 python tools/run_cfg3.py 2e6 3e7 > $OUT/prof_plain_tc.log 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sa_tc -c 1 \
     -o $OUT/prof_sa_tc_$TAG python tools/run_cfg3.py 2e6 3e7 > $OUT/ncu_full_tc.log 2>&1
 echo "full tc rc=$?" >> $OUT/ncu_full_tc.log
+# relabel engine (config 4 hot start) and the tensor-memory ensemble's scratch phase
+timeout 120 python tools/run_cfg.py 4 5e4 0 > $OUT/prof_plain_rlb.log 2>&1 && \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sa_relabel -c 1 \
+    -o $OUT/prof_relabel_$TAG python tools/run_cfg.py 4 5e4 0 > $OUT/ncu_full_rlb.log 2>&1
+echo "full relabel rc=$?" >> $OUT/ncu_full_rlb.log
+timeout 120 python tools/run_ens.py 1184 2e5 > $OUT/prof_plain_ens.log 2>&1 && \
+  timeout 900 ncu --set full --clock-control none -k regex:k_sa_scratch -c 1 \
+    -o $OUT/prof_ens_$TAG python tools/run_ens.py 1184 2e5 > $OUT/ncu_full_ens.log 2>&1
+echo "full ensemble rc=$?" >> $OUT/ncu_full_ens.log
