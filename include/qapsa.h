@@ -168,7 +168,11 @@ qap_status qap_schedule_bounds(qap_ctx* ctx, double* t0, double* tf);
  *      best_cost, ties to the lowest chain id;
  *  sum_stats (nullable): summed iterations/accepted/near_ties, digest =
  *      XOR of chain digests, cost/best_cost = those of best_chain;
- *  per_chain (nullable): chain_count results in chain order. */
+ *  per_chain (nullable): chain_count results in chain order.
+ * Engine: on instances the tensor-memory engine takes (and QAP_OPT_TENSOR_CORE = 1,
+ * QAP_OPT_PROPOSAL = 0) the single-chain tensor-memory kernels run over all chains, one CTA
+ * per chain (two per SM in the scratch phase); otherwise the shared-memory kernel runs several
+ * chains per CTA (QAP_OPT_ENSEMBLE_GROUP threads each).  Same results either way. */
 qap_status qap_ensemble_run(qap_ctx* ctx, uint32_t chain_begin, uint32_t chain_count,
                             const int32_t* p0s, uint64_t iters, const qap_schedule* s,
                             uint64_t seed, int64_t* best_cost, uint32_t* best_chain,
