@@ -113,10 +113,12 @@ qap_status qap_create(int32_t n, const int32_t* A, const int32_t* B, const int32
 /* Frees all device memory of ctx (NULL is a no-op). */
 void qap_destroy(qap_ctx* ctx);
 
-/* qap_reset -- p = perm (n int32 host array) or, if perm is NULL, the p0 of
- * qap_create, kept on the device (no host transfer).  Recomputes B', C,
- * best = C, best_p = p, digest seed, clears the near-tie log; Δ becomes
- * invalid until qap_delta_init. */
+/* qap_reset -- restart the chain from an assignment: "an initial assignment
+ * p" (step (a)) and B' = B[p][p] (R9).  p = perm (n int32 host
+ * array) or, if perm is NULL, the p0 of qap_create, kept on the device (no
+ * host transfer).  Recomputes B', C = Eq.(1), best = C, best_p = p
+ * (R17), digest seed (R18), clears the near-tie log; Δ becomes invalid until
+ * qap_delta_init.  Errors: QAP_E_DIMENSION if perm is not a permutation. */
 qap_status qap_reset(qap_ctx* ctx, const int32_t* perm);
 
 /* qap_delta_init -- step (a) of P:46: Δ_rs for every pair r < s at the
@@ -140,15 +142,21 @@ qap_status qap_sa_run(qap_ctx* ctx, uint64_t k0, uint64_t iters, const qap_sched
  * the device in int64. */
 qap_status qap_cost(qap_ctx* ctx, const int32_t* perm, int64_t* out);
 
-/* qap_get_state -- copies the current p, best_p (n int32 each) and Δ
- * (M int32, layout above) to host buffers; any of them may be NULL.
+/* qap_get_state -- the outputs of step (e) ("end after I iterations"):
+ * copies the current assignment p, the best assignment best_p (R17; n int32
+ * each) and the swap-cost matrix Δ (M int32, layout above) to
+ * caller-owned host buffers; any of them may be NULL.
  * delta != NULL requires a valid Δ (QAP_E_STATE otherwise). */
 qap_status qap_get_state(qap_ctx* ctx, int32_t* perm, int32_t* best_perm, int32_t* delta);
 
-/* qap_get_near_ties -- iterations k flagged as near ties since the last
- * reset with the decision the device took (1 = accepted), in the order they
- * were logged, up to cap entries; *count receives the total number flagged
- * (may exceed cap; only the first QAP_NEAR_LOG_CAP are kept). */
+/* qap_get_near_ties -- Eq.(2) evaluated in double precision can be
+ * decided differently by two correct implementations only when
+ * |delta + T ln r| is within rounding of 0 (R16, BASELINE north_star): those
+ * iterations k (delta > 0, |delta + T ln r| < 1e-9 T) flagged since the last
+ * reset, with the decision the device took (1 = accepted), in the order they
+ * were logged, up to cap entries (ks: cap uint64, decisions: cap uint8, host);
+ * *count receives the total number flagged (may exceed cap; only the first
+ * QAP_NEAR_LOG_CAP are kept). */
 #define QAP_NEAR_LOG_CAP 1024
 qap_status qap_get_near_ties(qap_ctx* ctx, uint64_t* ks, uint8_t* decisions, int32_t cap,
                              int32_t* count);
@@ -159,11 +167,14 @@ qap_status qap_get_near_ties(qap_ctx* ctx, uint64_t* ks, uint8_t* decisions, int
  * Requires a valid Δ. */
 qap_status qap_schedule_bounds(qap_ctx* ctx, double* t0, double* tf);
 
-/* qap_ensemble_run -- independent chains (BASELINE config 5) on the
- * context's instance: chains with GLOBAL ids chain_begin .. chain_begin +
- * chain_count - 1, chain c starting from p0s[(c - chain_begin) * n ...],
- * each running iterations 0 .. iters-1 of *s with r_k keyed by (seed, k, c)
- * (R3, R18).  The context's single-chain state is not touched.
+/* qap_ensemble_run -- independent chains ("run copies of the heuristic
+ * independently"; BASELINE config 5) on the context's instance: chains with
+ * GLOBAL ids chain_begin .. chain_begin + chain_count - 1, each running
+ * iterations 0 .. iters-1 of *s with r_k keyed by (seed, k, c) (R3, R19).
+ * Chain c starts from p0s[(c - chain_begin) * n ...] (chain_count*n int32,
+ * host) or, if p0s is NULL, from the chain-keyed Fisher-Yates permutation
+ * generated on the device (qap_start_perms(seed, c), R14b): no host array.
+ * The context's single-chain state is not touched.
  *  best_cost/best_chain/best_perm (n int32): argmin over these chains of
  *      best_cost, ties to the lowest chain id;
  *  sum_stats (nullable): summed iterations/accepted/near_ties, digest =
@@ -178,6 +189,24 @@ qap_status qap_ensemble_run(qap_ctx* ctx, uint32_t chain_begin, uint32_t chain_c
                             uint64_t seed, int64_t* best_cost, uint32_t* best_chain,
                             int32_t* best_perm, qap_stats* sum_stats,
                             qap_chain_result* per_chain);
+
+/* qap_ensemble_near_ties -- the near ties (R16, see qap_get_near_ties) of the
+ * last qap_ensemble_run, every entry with its GLOBAL chain id, so that each
+ * flagged chain can be replayed with the device's decisions.  chains (uint32),
+ * ks (uint64), decisions (uint8): cap entries each, host; *count = the total
+ * flagged in that run (only the first QAP_ENS_NEAR_LOG_CAP are kept). */
+#define QAP_ENS_NEAR_LOG_CAP 65536
+qap_status qap_ensemble_near_ties(qap_ctx* ctx, uint32_t* chains, uint64_t* ks, uint8_t* decisions,
+                                  int32_t cap, int32_t* count);
+
+/* qap_start_perms -- initial assignments of independent chains (P:46 step (a)
+ * "an initial assignment p"): chain c = chain_begin .. chain_begin +
+ * count - 1 gets the Fisher-Yates shuffle of the identity with, for
+ * i = n-1 .. 1, j = floor(x (i+1) / 2^32), x = Philox4x32-10(key = seed,
+ * ctr = (i, 0, c, tag 1)).x, swap p[i], p[j] (R14b), computed on
+ * the device.  out: count*n int32 host buffer, row c - chain_begin = p of c. */
+qap_status qap_start_perms(qap_ctx* ctx, uint64_t seed, uint32_t chain_begin, uint32_t count,
+                           int32_t* out);
 
 /* Tuning knobs.  Results never depend on them (window / CTA shape
  * invariance); they exist for the invariance tests and benchmarks. */

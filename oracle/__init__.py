@@ -82,9 +82,10 @@ def lib():
             C.c_uint64, C.c_uint64, C.c_uint32,
             C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int64]
         L.orc_sa_run.restype = C.c_int
-        L.orc_ensemble_run.argtypes = [C.c_int, _i32p, _i32p, _i32p, C.c_int64, C.c_uint32,
+        L.orc_ensemble_run.argtypes = [C.c_int, _i32p, _i32p, C.c_void_p, C.c_int64, C.c_uint32,
                                        C.c_uint64, C.c_int, C.c_double, C.c_double, C.c_uint64,
-                                       C.c_int, _i64p]
+                                       C.c_int, C.c_int, _i64p, C.c_void_p, C.c_void_p, C.c_int]
+        L.orc_start_perm.argtypes = [C.c_int, C.c_uint64, C.c_uint32, _i32p]
         L.orc_ensemble_run.restype = C.c_int
         _lib = L
     return _lib
@@ -235,16 +236,38 @@ class Run:
                     near_ties=s.near_ties, iterations=s.iterations)
 
 
-def ensemble_run(A, B, p0s, chain_base, iters, sched: Schedule, seed, threads=None):
-    """Per-chain results (count, 6): cost, best_cost, accepted, near_ties, digest, iterations."""
+def start_perm(n, seed, chain):
+    """Chain-keyed Fisher-Yates start permutation (SURVEY §8(c) c3 #14, DESIGN.md R14b)."""
+    p = np.zeros(n, np.int32)
+    lib().orc_start_perm(n, seed, chain, p)
+    return p
+
+
+def ensemble_run(A, B, p0s, chain_base, iters, sched: Schedule, seed, threads=None,
+                 mode=MODE_DELTA, count=None, near_cap=0):
+    """Per-chain results (count, 6): cost, best_cost, accepted, near_ties, digest, iterations.
+    p0s None: chain c starts from start_perm(n, seed, c) (then `count` is required).
+    near_cap > 0: also returns the per-chain near-tie logs, a list of [(k, decision), ...]."""
     A = _i32(A)
-    p0s = _i32(p0s)
-    count = p0s.shape[0]
+    n = A.shape[0]
+    if p0s is not None:
+        p0s = _i32(p0s)
+        count = p0s.shape[0]
     out = np.zeros((count, 6), np.int64)
+    nk = np.zeros(max(1, count * near_cap), np.uint64)
+    nd = np.zeros(max(1, count * near_cap), np.uint8)
     threads = threads or os.cpu_count() or 1
-    lib().orc_ensemble_run(A.shape[0], A, _i32(B), p0s, count, chain_base, iters, sched.kind,
-                           sched.t0, sched.tf, seed, threads, out)
-    return out
+    lib().orc_ensemble_run(n, A, _i32(B), p0s.ctypes.data if p0s is not None else None, count,
+                           chain_base, iters, sched.kind, sched.t0, sched.tf, seed, threads, mode,
+                           out, nk.ctypes.data if near_cap else None,
+                           nd.ctypes.data if near_cap else None, near_cap)
+    if not near_cap:
+        return out
+    logs = []
+    for c in range(count):
+        m = min(int(out[c, 3]), near_cap)
+        logs.append([(int(nk[c * near_cap + i]), int(nd[c * near_cap + i])) for i in range(m)])
+    return out, logs
 
 
 def geometric_schedule_for(A, B, p0, total_iters):

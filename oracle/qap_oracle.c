@@ -345,12 +345,31 @@ done:
 }
 
 /* ------------------------------------------------------------------ */
+/* Start permutation of a chain (R14b).  */
+/* ------------------------------------------------------------------ */
+/* Fisher-Yates from the identity (Knuth, TAOCP vol. 2, Algorithm 3.4.2 P): for i = n-1 down to 1,
+ * j = floor(x (i+1) / 2^32) with x the first word of Philox4x32-10(key = seed, ctr = (i, 0, chain,
+ * tag 1)), then swap p[i] and p[j].  j is uniform on 0..i up to the 2^-32 granularity of x. */
+void orc_start_perm(int n, uint64_t seed, uint32_t chain, int32_t* p) {
+    const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    for (int i = 0; i < n; ++i) p[i] = i;
+    for (int i = n - 1; i >= 1; --i) {
+        const uint32_t ctr[4] = {(uint32_t)i, 0u, chain, 1u};
+        uint32_t x[4];
+        orc_philox4x32_10(ctr, key, x);
+        const int j = (int)(((uint64_t)x[0] * (uint64_t)(i + 1)) >> 32);
+        const int32_t t = p[i]; p[i] = p[j]; p[j] = t;
+    }
+}
+
+/* ------------------------------------------------------------------ */
 /* Independent chains (BASELINE config 5) on host threads.       */
 /* ------------------------------------------------------------------ */
 typedef struct {
     int n; const int32_t* A; const int32_t* B; const int32_t* p0s;
     int64_t begin, end; uint64_t iters; int kind; double t0, tf; uint64_t seed;
-    uint32_t chain_base; int64_t* out; int64_t* next; pthread_mutex_t* lock;
+    uint32_t chain_base; int mode; int64_t* out; uint64_t* near_k; uint8_t* near_d; int near_cap;
+    int64_t* next; pthread_mutex_t* lock;
 } ens_job;
 
 static void* ens_worker(void* arg) {
@@ -358,36 +377,45 @@ static void* ens_worker(void* arg) {
     int n = j->n;
     int32_t* p = malloc(sizeof(int32_t) * n);
     int32_t* bp = malloc(sizeof(int32_t) * n);
+    int32_t* p0 = malloc(sizeof(int32_t) * n);
     int32_t* Bp = malloc(sizeof(int32_t) * n * n);
-    int64_t* D = malloc(sizeof(int64_t) * (size_t)n * (n - 1) / 2);
+    int64_t* D = malloc(sizeof(int64_t) * (size_t)(n * (n - 1) / 2 + 1));
     for (;;) {
         pthread_mutex_lock(j->lock);
         int64_t c = (*j->next)++;
         pthread_mutex_unlock(j->lock);
         if (c >= j->end) break;
-        orc_state st = {n, ORC_MODE_DELTA, j->A, j->B, p, bp, Bp, D, 0, 0, 0, 0, 0, 0, 0, 0};
-        orc_state_reset(&st, j->p0s + (size_t)(c - j->begin) * n);
-        orc_sa_run(&st, 0, j->iters, j->kind, j->t0, j->tf, j->iters, j->seed,
-                   j->chain_base + (uint32_t)(c - j->begin), NULL, NULL, 0, NULL, NULL, 0, 0);
+        const uint32_t chain = j->chain_base + (uint32_t)(c - j->begin);
+        if (j->p0s) memcpy(p0, j->p0s + (size_t)(c - j->begin) * n, sizeof(int32_t) * (size_t)n);
+        else orc_start_perm(n, j->seed, chain, p0);
+        orc_state st = {n, j->mode, j->A, j->B, p, bp, Bp, D, 0, 0, 0, 0, 0, 0, 0, 0};
+        orc_state_reset(&st, p0);
+        const size_t lo = (size_t)(c - j->begin) * (size_t)j->near_cap;
+        orc_sa_run(&st, 0, j->iters, j->kind, j->t0, j->tf, j->iters, j->seed, chain, NULL, NULL, 0,
+                   j->near_k ? j->near_k + lo : NULL, j->near_d ? j->near_d + lo : NULL, j->near_cap, 0);
         int64_t* o = j->out + (size_t)(c - j->begin) * 6;
         o[0] = st.cost; o[1] = st.best_cost; o[2] = (int64_t)st.accepted;
         o[3] = (int64_t)st.near_ties; o[4] = (int64_t)st.digest; o[5] = (int64_t)st.iterations;
     }
-    free(p); free(bp); free(Bp); free(D);
+    free(p); free(bp); free(p0); free(Bp); free(D);
     return NULL;
 }
 
-/* Runs chains chain_base .. chain_base+count-1 (start perms p0s, count*n),
- * each for iters iterations of its own schedule; out: count*6 int64
- * (cost, best_cost, accepted, near_ties, digest, iterations). */
+/* Runs chains chain_base .. chain_base+count-1, each for iters iterations of its own schedule,
+ * with δ taken from `mode` (ORC_MODE_*; all three give the same trajectory).  Start permutations:
+ * p0s (count*n) or, if p0s is NULL, orc_start_perm(seed, chain).  out: count*6 int64 (cost,
+ * best_cost, accepted, near_ties, digest, iterations); near_k/near_d (nullable, count*near_cap):
+ * each chain's first near_cap near ties (k, decision). */
 int orc_ensemble_run(int n, const int32_t* A, const int32_t* B, const int32_t* p0s, int64_t count,
                      uint32_t chain_base, uint64_t iters, int kind, double t0, double tf,
-                     uint64_t seed, int threads, int64_t* out) {
+                     uint64_t seed, int threads, int mode, int64_t* out, uint64_t* near_k,
+                     uint8_t* near_d, int near_cap) {
     if (threads < 1) threads = 1;
     pthread_t* th = malloc(sizeof(pthread_t) * threads);
     pthread_mutex_t lock = PTHREAD_MUTEX_INITIALIZER;
     int64_t next = 0;
-    ens_job job = {n, A, B, p0s, 0, count, iters, kind, t0, tf, seed, chain_base, out, &next, &lock};
+    ens_job job = {n, A, B, p0s, 0, count, iters, kind, t0, tf, seed, chain_base, mode, out,
+                   near_k, near_d, near_cap, &next, &lock};
     for (int t = 0; t < threads; ++t) pthread_create(&th[t], NULL, ens_worker, &job);
     for (int t = 0; t < threads; ++t) pthread_join(th[t], NULL);
     free(th);

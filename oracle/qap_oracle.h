@@ -92,13 +92,20 @@ int orc_sa_run(orc_state* st, uint64_t k0, uint64_t iters, int kind, double t0, 
                const uint64_t* follow_k, const uint8_t* follow_d, int n_follow,
                uint64_t* near_k, uint8_t* near_d, int near_cap, int64_t check_every);
 
+/* Start permutation of chain `chain` (R14b): Fisher-Yates from the
+ * identity, j = floor(x (i+1) / 2^32), x = Philox(key = seed; ctr = (i, 0, chain, tag 1)).x. */
+void orc_start_perm(int n, uint64_t seed, uint32_t chain, int32_t* p);
+
 /* Independent chains chain_base..chain_base+count-1 (BASELINE config 5)
- * on `threads` host threads, DELTA mode, each chain its own full schedule of
- * iters iterations.  out: count*6 int64 = (cost, best_cost, accepted,
- * near_ties, digest bits, iterations) per chain. */
+ * on `threads` host threads, δ source `mode`, each chain its own full schedule of
+ * iters iterations; p0s (count*n) or NULL = orc_start_perm(seed, chain).
+ * out: count*6 int64 = (cost, best_cost, accepted, near_ties, digest bits,
+ * iterations) per chain; near_k/near_d (nullable, count*near_cap): per-chain
+ * near-tie log (k, decision). */
 int orc_ensemble_run(int n, const int32_t* A, const int32_t* B, const int32_t* p0s, int64_t count,
                      uint32_t chain_base, uint64_t iters, int kind, double t0, double tf,
-                     uint64_t seed, int threads, int64_t* out);
+                     uint64_t seed, int threads, int mode, int64_t* out, uint64_t* near_k,
+                     uint8_t* near_d, int near_cap);
 
 #ifdef __cplusplus
 }

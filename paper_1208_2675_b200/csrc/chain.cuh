@@ -114,12 +114,30 @@ struct ChainScalars {  // meaningful in thread scalar_tid(NT, n) of the group
     uint64_t digest;
 };
 
-struct NearSink {      // global near-tie log (single chain) or nullptr
+// Near-tie sink (R16).  Single chain: count = the context's counter, log (ks, dec) indexed by it.
+// Ensembles: count = the chain's own counter (or nullptr), lcount = the launch-wide log counter,
+// and every entry also records the chain id, so a flagged chain can be followed by the oracle.
+struct NearSink {
     unsigned int* count;
     unsigned long long* ks;
     unsigned char* dec;
     int cap;
+    unsigned int* lcount;
+    uint32_t* lchain;
+    uint32_t chain;
 };
+
+// records near tie (k, decision) of a consumed iteration
+__device__ __forceinline__ void near_record(const NearSink& s, uint64_t k, bool dec) {
+    unsigned int e = 0;
+    if (s.count) e = atomicAdd(s.count, 1u);
+    if (s.lcount) e = atomicAdd(s.lcount, 1u);
+    if (s.ks && (int)e < s.cap) {
+        s.ks[e] = (unsigned long long)k;
+        s.dec[e] = dec ? 1 : 0;
+        if (s.lchain) s.lchain[e] = s.chain;
+    }
+}
 
 __device__ __forceinline__ int round_up32(int x) { return (x + 31) & ~31; }
 
@@ -296,7 +314,7 @@ __device__ __forceinline__ void prepare_theta(Prep& pr, const Sched& sch, uint64
     const U4 x = philox4x32_10((uint32_t)kk, (uint32_t)(kk >> 32), chain, 0u, (uint32_t)seed,
                                (uint32_t)(seed >> 32));
     const uint64_t bits = ((uint64_t)x.y << 32) | (uint64_t)x.x;
-    const float rf = __ull2float_rn(bits >> 11) * 0x1p-53f;   // r_k in float (> 0)
+    const float rf = (__ull2float_rn(bits >> 11) + 0.5f) * 0x1p-53f;   // r_k of R3 in float (> 0)
     const float T = temp32(sch, kk);
     pr.th = T * -__logf(rf);                                   // >= 0
     pr.m = 2e-4f * pr.th + 2e-5f * T;
@@ -442,13 +460,7 @@ __device__ __forceinline__ uint64_t chain_run(const TA* __restrict__ A, const Ch
         const int consumed = (j == INT_MAX) ? Wl : j + 1;
         if (near && off < consumed) {             // R16: count / log near ties of consumed iterations
             atomicAdd(&cs.flags[1], 1);
-            if (sink.count) {
-                const unsigned int i = atomicAdd(sink.count, 1u);
-                if ((int)i < sink.cap) {
-                    sink.ks[i] = (unsigned long long)(k + (uint64_t)off);
-                    sink.dec[i] = acc ? 1 : 0;
-                }
-            }
+            near_record(sink, k + (uint64_t)off, acc);
         }
         if (j == INT_MAX) {                       // no accepted swap in the window
             PT_ADD(1, pt0, pt1);

@@ -226,6 +226,8 @@ struct ChainArgs {
     // ensemble launches of the tensor-memory kernels (ens = 1): CTA b runs chain chain + b on
     // p + b n, best_p + b n, st + b, D + b dstride, k0_dev + 2 b; near ties only counted
     int ens, dstride;
+    uint32_t* near_chain;    // ensembles: chain id of every near-tie log entry (near_count = the
+                             // launch-wide log counter, near_k / near_dec the log)
     uint32_t chain;          // Philox chain id (R3) of the chain (of CTA 0 when ens)
     unsigned long long switch_gap;   // scratch phase: switch to Δ after this many iterations
                                      // without an accept (0 = TCS_SWITCH_GAP)
@@ -248,7 +250,7 @@ __device__ __forceinline__ ChainView chain_view(const ChainArgs& a) {
     ChainView v;
     if (!ENS) {
         v.p = a.p; v.best_p = a.best_p; v.D = a.D; v.st = a.st; v.k0_dev = a.k0_dev;
-        v.sink = NearSink{a.near_count, a.near_k, a.near_dec, a.near_cap};
+        v.sink = NearSink{a.near_count, a.near_k, a.near_dec, a.near_cap, nullptr, nullptr, 0u};
         v.chain = 0u;
         return v;
     }
@@ -258,8 +260,8 @@ __device__ __forceinline__ ChainView chain_view(const ChainArgs& a) {
     v.D = a.D + (size_t)b * a.dstride;
     v.st = a.st + b;
     v.k0_dev = a.k0_dev ? a.k0_dev + 2 * b : nullptr;
-    v.sink = NearSink{&v.st->near_count, nullptr, nullptr, 0};
     v.chain = a.chain + (uint32_t)b;
+    v.sink = NearSink{&v.st->near_count, a.near_k, a.near_dec, a.near_cap, a.near_count, a.near_chain, v.chain};
     return v;
 }
 
@@ -299,7 +301,7 @@ __global__ void __launch_bounds__(NT, 1) k_sa_chain(const ChainArgs a) {
     chain_diag_init<TA, TB, NT>(As, cs, n, ld, t);
     __syncthreads();
 
-    const NearSink sink{a.near_count, a.near_k, a.near_dec, a.near_cap};
+    const NearSink sink{a.near_count, a.near_k, a.near_dec, a.near_cap, nullptr, nullptr, 0u};
     constexpr int QPT = NFIX ? quads_per_thread(NT, NFIX) : 0;
     const uint64_t acc = chain_run<TA, TB, NT, QPT>(As, cs, tb, n, ld, M, nqt, a.k0, a.k_end, a.sch,
                                                     a.seed, 0u, 0, t, a.wmax, io, sink, a.proposal != 0);
@@ -333,6 +335,11 @@ struct EnsArgs {
     unsigned long long iters, seed;
     Sched sch;
     int proposal;            // 0 sequential enumeration (R4), 1 random pairs (R22)
+    unsigned int* near_count;    // launch-wide near-tie log (chain, k, decision), capacity near_cap
+    unsigned long long* near_k;
+    unsigned char* near_dec;
+    uint32_t* near_chain;
+    int near_cap;
 };
 
 template <typename TA, typename TB, int NT, int NFIX>
@@ -388,7 +395,8 @@ __global__ void __launch_bounds__(1024, 1) k_ensemble(const EnsArgs a) {
         for (int w = 0; w < NT / 32; ++w) io.cost += red[w];
         io.best = io.cost;
         group_sync(bar, NT);
-        const NearSink sink{nullptr, nullptr, nullptr, 0};
+        const NearSink sink{nullptr, a.near_k, a.near_dec, a.near_cap, a.near_count, a.near_chain,
+                            a.chain_begin + (unsigned)ci};
         constexpr int QPT = NFIX ? quads_per_thread(NT, NFIX) : 0;
         const uint64_t acc = chain_run<TA, TB, NT, QPT>(As, cs, tb, n, ld, M, nqt, 0ull, a.iters, a.sch,
                                                    a.seed, a.chain_begin + (unsigned)ci, bar, t,
@@ -405,6 +413,24 @@ __global__ void __launch_bounds__(1024, 1) k_ensemble(const EnsArgs a) {
             a.res[ci] = r;
         }
         group_sync(bar, NT);
+    }
+}
+
+// Chain-keyed start permutations (R14b), one thread per chain:
+// Fisher-Yates from the identity, for i = n-1 .. 1: j = floor(x (i+1) / 2^32) with
+// x = Philox4x32-10(key = seed, ctr = (i, 0, chain, tag 1)).x, then swap p[i], p[j].
+__global__ void k_start_perms(int n, unsigned long long seed, uint32_t chain_begin, int count, int32_t* out) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= count) return;
+    int32_t* p = out + (size_t)c * n;
+    for (int i = 0; i < n; ++i) p[i] = i;
+    for (int i = n - 1; i >= 1; --i) {
+        const U4 x = philox4x32_10((uint32_t)i, 0u, chain_begin + (uint32_t)c, 1u, (uint32_t)seed,
+                                   (uint32_t)(seed >> 32));
+        const int j = (int)(((uint64_t)x.x * (uint64_t)(i + 1)) >> 32);
+        const int32_t t = p[i];
+        p[i] = p[j];
+        p[j] = t;
     }
 }
 

@@ -72,6 +72,11 @@ struct qap_ctx {
     uint8_t* dcls = nullptr;            // n
     uint16_t* dpt = nullptr;            // ncls x (n+1)
     int32_t* dD2 = nullptr;             // quad layout, same size as dD
+    // near-tie log of the last qap_ensemble_run: (chain, k, decision), R16
+    unsigned int* ens_near_count = nullptr;
+    unsigned long long* ens_near_k = nullptr;
+    unsigned char* ens_near_dec = nullptr;
+    uint32_t* ens_near_chain = nullptr;
 };
 
 static thread_local std::string g_static_err;
@@ -260,7 +265,8 @@ void qap_destroy(qap_ctx* c) {
                     c->dqdesc, c->dst, c->dnear_count,
                     c->dnear_k, c->dnear_dec, c->dscratch, c->ens_p0, c->ens_res, c->ens_best,
                     c->ens_counter, c->dkout, c->dcls, c->dpt, c->dD2, c->tp, c->tbp, c->tD,
-                    c->tst, c->tkout};
+                    c->tst, c->tkout, c->ens_near_count, c->ens_near_k, c->ens_near_dec,
+                    c->ens_near_chain};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->ev0) cudaEventDestroy(c->ev0);
@@ -356,6 +362,10 @@ qap_status qap_create(int32_t n, const int32_t* A, const int32_t* B, const int32
     alloc((void**)&c->dscratch, 8 * sizeof(long long));
     alloc((void**)&c->dkout, 2 * sizeof(unsigned long long));
     alloc((void**)&c->dD2, (size_t)c->nqt * 16 + 16);
+    alloc((void**)&c->ens_near_count, sizeof(unsigned int));
+    alloc((void**)&c->ens_near_k, QAP_ENS_NEAR_LOG_CAP * sizeof(unsigned long long));
+    alloc((void**)&c->ens_near_dec, QAP_ENS_NEAR_LOG_CAP);
+    alloc((void**)&c->ens_near_chain, QAP_ENS_NEAR_LOG_CAP * sizeof(uint32_t));
     std::vector<uint8_t> hcls;
     std::vector<uint16_t> hpt;
     twin_classes(n, A, &hcls, &hpt, &c->ncls);
@@ -378,6 +388,7 @@ qap_status qap_create(int32_t n, const int32_t* A, const int32_t* B, const int32
     if (e == cudaSuccess) e = cudaMemcpyAsync(c->dcls, hcls.data(), n, cudaMemcpyHostToDevice, c->stream);
     if (e == cudaSuccess && !hpt.empty()) e = cudaMemcpyAsync(c->dpt, hpt.data(), hpt.size() * 2, cudaMemcpyHostToDevice, c->stream);
     if (e == cudaSuccess) e = cudaMemsetAsync(c->dD2, 0, (size_t)c->nqt * 16 + 16, c->stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(c->ens_near_count, 0, sizeof(unsigned int), c->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);   // host tables go out of scope
     if (e != cudaSuccess) {
         std::string m = cudaGetErrorString(e);
@@ -450,7 +461,6 @@ static cudaError_t launch_generic(qap_ctx* c, const ChainArgs& a, bool ds, int s
               : launch_chain_t<TA, TB, NT, false, 0>(c, a, smem);
 }
 
-// Threads of the single-chain CTA: enough for 4 lanes per touching v and <= 3 quads per thread.
 // Threads of the single-chain CTA: touching warps (8 v each) plus quad warps with
 // <= 4 quads per thread, rounded to a power of two.
 static int auto_threads(const qap_ctx* c) {
@@ -528,6 +538,7 @@ qap_status qap_sa_run(qap_ctx* c, uint64_t k0, uint64_t iters, const qap_schedul
     a.rowaddr = c->drowaddr; a.qdesc = c->dqdesc; a.nqt = c->nqt;
     a.near_count = c->dnear_count; a.near_k = c->dnear_k; a.near_dec = c->dnear_dec;
     a.near_cap = QAP_NEAR_LOG_CAP;
+    a.near_chain = nullptr;
     a.n = c->n; a.ld = c->ld; a.M = c->M; a.wmax = std::min(c->wmax, threads);
     a.k0 = k0; a.k_end = k0 + iters; a.seed = seed; a.sch = sch;
 
@@ -722,10 +733,6 @@ static cudaError_t launch_ens(qap_ctx* c, const EnsArgs& a, int nt, int groups, 
     return launch_ens_t<uint16_t, uint16_t, 128, 0>(c, a, groups, smem);
 }
 
-extern "C" {
-
-}  // extern "C"
-
 // Ensemble on the tensor-memory engine: one CTA per chain, the single-chain kernels launched over
 // all chains at once -- the scratch phase (two chains per SM: 256 TMEM columns each), the Δ
 // rebuild of every chain, the Δ engine (one chain per SM) -- then the per-chain results and the
@@ -761,11 +768,13 @@ static qap_status ensemble_tc(qap_ctx* c, uint32_t chain_begin, uint32_t chain_c
             return fail(c, QAP_E_NOMEM, "tensor-memory ensemble buffers");
         c->tcap = chain_count;
     }
-    CU(cudaMemcpyAsync(c->ens_p0, p0s, (size_t)chain_count * n * 4, cudaMemcpyHostToDevice, c->stream));
+    if (p0s) CU(cudaMemcpyAsync(c->ens_p0, p0s, (size_t)chain_count * n * 4, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemsetAsync(c->ens_near_count, 0, sizeof(unsigned int), c->stream));
     ChainArgs a;
     a.A = c->dA; a.B = c->dB; a.p = c->tp; a.best_p = c->tbp; a.D = c->tD; a.st = c->tst;
     a.rowaddr = c->drowaddr; a.qdesc = c->dqdesc; a.nqt = c->nqt;
-    a.near_count = nullptr; a.near_k = nullptr; a.near_dec = nullptr; a.near_cap = 0;
+    a.near_count = c->ens_near_count; a.near_k = c->ens_near_k; a.near_dec = c->ens_near_dec;
+    a.near_chain = c->ens_near_chain; a.near_cap = QAP_ENS_NEAR_LOG_CAP;
     a.n = n; a.ld = c->ld; a.M = c->M; a.wmax = c->wmax;
     a.k0 = 0; a.k_end = iters; a.seed = seed; a.sch = sch;
     a.k0_dev = nullptr; a.proposal = 0;
@@ -774,6 +783,10 @@ static qap_status ensemble_tc(qap_ctx* c, uint32_t chain_begin, uint32_t chain_c
     // phase (config 5: gap 4096 / 16384 / 65536 / never = 3.67 / 3.64 / 3.62 / 3.66 s)
     a.switch_gap = 65536;
     CU(cudaEventRecord(c->ev0, c->stream));
+    if (!p0s) {                                  // chain-keyed start permutations on the device (R14b)
+        k_start_perms<<<(chain_count + 127) / 128, 128, 0, c->stream>>>(n, seed, chain_begin, (int)chain_count, c->ens_p0);
+        CU(cudaGetLastError());
+    }
     k_reset<uint8_t, uint8_t><<<chain_count, 512, 0, c->stream>>>((const uint8_t*)c->dA, (const uint8_t*)c->dB,
                                                                    c->ens_p0, n, c->ld, c->tp, c->tbp, c->tst);
     CU(cudaGetLastError());
@@ -786,9 +799,13 @@ static qap_status ensemble_tc(qap_ctx* c, uint32_t chain_begin, uint32_t chain_c
     ks<<<chain_count, TCS_NT, ssm, c->stream>>>(a, c->tkout);
     CU(cudaGetLastError());
     const int dt = 256, db = (c->M + dt - 1) / dt;
-    k_delta_init<uint8_t, uint8_t><<<dim3(db, chain_count), dt, 0, c->stream>>>(
-        (const uint8_t*)c->dA, (const uint8_t*)c->dB, c->tp, c->drowaddr, n, c->ld, c->M, c->tD, dstride);
-    CU(cudaGetLastError());
+    for (uint32_t c0 = 0; c0 < chain_count; c0 += 65535u) {   // gridDim.y <= 65535: slices of chains
+        const uint32_t cs = std::min<uint32_t>(65535u, chain_count - c0);
+        k_delta_init<uint8_t, uint8_t><<<dim3(db, cs), dt, 0, c->stream>>>(
+            (const uint8_t*)c->dA, (const uint8_t*)c->dB, c->tp + (size_t)c0 * n, c->drowaddr, n, c->ld, c->M,
+            c->tD + (size_t)c0 * dstride, dstride);
+        CU(cudaGetLastError());
+    }
     a.k0_dev = c->tkout;
     auto kern = n == 100 ? k_sa_tc<100, true> : n == 50 ? k_sa_tc<50, true> : n == 12 ? k_sa_tc<12, true>
               : k_sa_tc<0, true>;
@@ -822,7 +839,7 @@ static qap_status ensemble_tc(qap_ctx* c, uint32_t chain_begin, uint32_t chain_c
     if (per_chain)
         CU(cudaMemcpy(per_chain, c->ens_res, (size_t)chain_count * sizeof(ChainResult), cudaMemcpyDeviceToHost));
     CU(cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1));
-    c->last_launches = 4;
+    c->last_launches = 4 + (p0s ? 0 : 1) + (int)((chain_count - 1) / 65535u);
     return QAP_OK;
 }
 
@@ -833,14 +850,15 @@ qap_status qap_ensemble_run(qap_ctx* c, uint32_t chain_begin, uint32_t chain_cou
                             uint32_t* best_chain, int32_t* best_perm, qap_stats* sum_stats,
                             qap_chain_result* per_chain) {
     CHECK_CTX(c);
-    if (!p0s || !best_cost || !best_chain || !best_perm) return fail(c, QAP_E_INVALID_ARG, "NULL argument");
+    if (!best_cost || !best_chain || !best_perm) return fail(c, QAP_E_INVALID_ARG, "NULL argument");
     if (chain_count == 0 || iters == 0) return fail(c, QAP_E_INVALID_ARG, "chain_count or iters is 0");
     Sched sch;
     qap_status vs = validate_schedule(c, s, 0, iters, &sch);
     if (vs != QAP_OK) return vs;
     const int n = c->n;
-    for (uint32_t i = 0; i < chain_count; ++i)
-        if (!is_perm(n, p0s + (size_t)i * n)) return fail(c, QAP_E_DIMENSION, "a start permutation is invalid");
+    if (p0s)
+        for (uint32_t i = 0; i < chain_count; ++i)
+            if (!is_perm(n, p0s + (size_t)i * n)) return fail(c, QAP_E_DIMENSION, "a start permutation is invalid");
     if (use_tc_engine(c))
         return ensemble_tc(c, chain_begin, chain_count, p0s, iters, sch, seed, best_cost, best_chain,
                            best_perm, sum_stats, per_chain);
@@ -864,15 +882,22 @@ qap_status qap_ensemble_run(qap_ctx* c, uint32_t chain_begin, uint32_t chain_cou
         c->ens_cap = chain_count;
     }
     if (!c->ens_counter) CU(cudaMalloc(&c->ens_counter, sizeof(unsigned int)));
-    CU(cudaMemcpyAsync(c->ens_p0, p0s, (size_t)chain_count * n * 4, cudaMemcpyHostToDevice, c->stream));
+    if (p0s) CU(cudaMemcpyAsync(c->ens_p0, p0s, (size_t)chain_count * n * 4, cudaMemcpyHostToDevice, c->stream));
     CU(cudaMemsetAsync(c->ens_counter, 0, sizeof(unsigned int), c->stream));
+    CU(cudaMemsetAsync(c->ens_near_count, 0, sizeof(unsigned int), c->stream));
     EnsArgs a;
     a.A = c->dA; a.B = c->dB; a.p0s = c->ens_p0; a.res = c->ens_res; a.best_perms = c->ens_best;
     a.next_chain = c->ens_counter; a.count = (int)chain_count; a.n = n; a.ld = c->ld; a.M = c->M;
     a.rowaddr = c->drowaddr; a.qdesc = c->dqdesc; a.nqt = c->nqt;
     a.proposal = c->proposal;
     a.wmax = std::min(c->wmax, nt); a.chain_begin = chain_begin; a.iters = iters; a.seed = seed; a.sch = sch;
+    a.near_count = c->ens_near_count; a.near_k = c->ens_near_k; a.near_dec = c->ens_near_dec;
+    a.near_chain = c->ens_near_chain; a.near_cap = QAP_ENS_NEAR_LOG_CAP;
     CU(cudaEventRecord(c->ev0, c->stream));
+    if (!p0s) {                                  // chain-keyed start permutations on the device (R14b)
+        k_start_perms<<<(chain_count + 127) / 128, 128, 0, c->stream>>>(n, seed, chain_begin, (int)chain_count, c->ens_p0);
+        CU(cudaGetLastError());
+    }
     CU(launch_ens(c, a, nt, groups, smem));
     CU(cudaEventRecord(c->ev1, c->stream));
     k_ens_reduce<<<1, 1024, 0, c->stream>>>(c->ens_res, (int)chain_count, c->dscratch);
@@ -899,7 +924,43 @@ qap_status qap_ensemble_run(qap_ctx* c, uint32_t chain_begin, uint32_t chain_cou
         CU(cudaMemcpy(per_chain, c->ens_res, (size_t)chain_count * sizeof(ChainResult), cudaMemcpyDeviceToHost));
     }
     CU(cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1));
-    c->last_launches = 2;
+    c->last_launches = 2 + (p0s ? 0 : 1);
+    return QAP_OK;
+}
+
+qap_status qap_ensemble_near_ties(qap_ctx* c, uint32_t* chains, uint64_t* ks, uint8_t* decisions, int32_t cap,
+                                  int32_t* count) {
+    CHECK_CTX(c);
+    if (cap < 0 || !count || (cap > 0 && (!chains || !ks || !decisions)))
+        return fail(c, QAP_E_INVALID_ARG, "bad near-tie buffers");
+    CU(cudaSetDevice(c->dev));
+    unsigned int cnt = 0;
+    CU(cudaMemcpyAsync(&cnt, c->ens_near_count, sizeof cnt, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    const int m = std::min<int>(std::min<unsigned>(cnt, QAP_ENS_NEAR_LOG_CAP), cap);
+    if (m > 0) {
+        CU(cudaMemcpyAsync(chains, c->ens_near_chain, m * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+        CU(cudaMemcpyAsync(ks, c->ens_near_k, m * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
+        CU(cudaMemcpyAsync(decisions, c->ens_near_dec, m, cudaMemcpyDeviceToHost, c->stream));
+        CU(cudaStreamSynchronize(c->stream));
+    }
+    *count = (int32_t)cnt;
+    return QAP_OK;
+}
+
+qap_status qap_start_perms(qap_ctx* c, uint64_t seed, uint32_t chain_begin, uint32_t count, int32_t* out) {
+    CHECK_CTX(c);
+    if (!out || count == 0) return fail(c, QAP_E_INVALID_ARG, "out is NULL or count is 0");
+    CU(cudaSetDevice(c->dev));
+    int32_t* d = nullptr;
+    CU(cudaMallocAsync(&d, (size_t)count * c->n * 4, c->stream));
+    k_start_perms<<<(count + 127) / 128, 128, 0, c->stream>>>(c->n, seed, chain_begin, (int)count, d);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out, d, (size_t)count * c->n * 4, cudaMemcpyDeviceToHost, c->stream);
+    cudaFreeAsync(d, c->stream);
+    CU(e);
+    CU(cudaStreamSynchronize(c->stream));
+    c->last_launches = 1;
     return QAP_OK;
 }
 

@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
         else cl_store(loc, own, v);
     };
     bool pend_wait = false;                               // CL > 1: writes of the last update
-    const NearSink sink{a.near_count, a.near_k, a.near_dec, a.near_cap};
+    const NearSink sink{a.near_count, a.near_k, a.near_dec, a.near_cap, nullptr, nullptr, 0u};
     int64_t cost = a.st->cost, best = a.st->best_cost;   // scalar thread (t == RLB_NT - 1)
     uint64_t my_dig = 0, my_cnt = 0;                     // this thread's accepts (digest is a sum)
     uint64_t k = a.k0;
@@ -346,11 +346,7 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
         const unsigned below = lo >= 32 ? 0xffffffffu : (lo <= 0 ? 0u : ((1u << lo) - 1u));
         const bool any_twin = __reduce_or_sync(0xffffffffu, twm[lane] & below) != 0u;
         if (near && t < cons && crank == 0) {             // R16: near ties of consumed iterations
-            const unsigned int i = atomicAdd(sink.count, 1u);
-            if ((int)i < sink.cap) {
-                sink.ks[i] = (unsigned long long)(k + (uint64_t)t);
-                sink.dec[i] = acc ? 1 : 0;
-            }
+            near_record(sink, k + (uint64_t)t, acc);
         }
         if (twin && t < cons) {                           // relabel: σ rotated, accept counted
             const uint16_t old = sig[s];

@@ -192,8 +192,15 @@ __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, uns
         uint32_t gv[4], hf[4];                   // G[v][p(u_i)] (location lane v), H[f][u_i] (facility lane f = v)
 #pragma unroll
         for (int i = 0; i < 4; ++i) tc::tmem_ld1(tm + quad_lane + TCS_COL_G + (uint32_t)pu[i], gv[i]);
-        tc::tmem_ld4(tm + quad_lane + TCS_COL_H + (uint32_t)u0, hf);
+        // H columns u0 .. u0+3 must stay inside [TCS_COL_H, TCS_COL_H + 128) (an ensemble CTA owns
+        // only 256 columns): read from hb = min(u0, 124) and shift (rows past n-1 are never used)
+        const int hb = min(u0, 124), hsh = u0 - hb;
+        tc::tmem_ld4(tm + quad_lane + TCS_COL_H + (uint32_t)hb, hf);
         tc::tmem_wait_ld();
+        if (hsh) {                               // warp-uniform, only in the last rows of the triangle
+#pragma unroll
+            for (int i = 0; i < 3; ++i) hf[i] = hsh == 1 ? hf[i + 1] : (i < 2 ? hf[i + 2] : hf[3]);
+        }
         if (vin) {
 #pragma unroll
             for (int i = 0; i < 4; ++i) xch[i * 128 + qv] = (int)hf[i];   // G[u_i][v] to location p^-1(v)
@@ -264,11 +271,7 @@ __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, uns
             for (int i = 0; i < 4; ++i) {
                 const int o = rb[i] + v;
                 if (((near_mask >> i) & 1u) && o < consumed) {
-                    const unsigned int e = atomicAdd(sink.count, 1u);
-                    if ((int)e < sink.cap) {
-                        sink.ks[e] = (unsigned long long)(k + (uint64_t)o);
-                        sink.dec[e] = (unsigned char)((acc_mask >> i) & 1u);
-                    }
+                    near_record(sink, k + (uint64_t)o, (acc_mask >> i) & 1u);
                 }
             }
         }

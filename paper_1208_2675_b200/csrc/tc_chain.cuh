@@ -398,11 +398,7 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
             for (int i = 0; i < 8; ++i) {
                 const int o = rb[i] + v;
                 if (((near_mask >> i) & 1u) && o < consumed) {
-                    const unsigned int e = atomicAdd(sink.count, 1u);
-                    if ((int)e < sink.cap) {
-                        sink.ks[e] = (unsigned long long)(k + (uint64_t)o);
-                        sink.dec[e] = (unsigned char)((acc_mask >> i) & 1u);
-                    }
+                    near_record(sink, k + (uint64_t)o, (acc_mask >> i) & 1u);
                 }
             }
         }

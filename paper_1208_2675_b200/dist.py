@@ -38,15 +38,16 @@ class EnsembleResult:
 
 
 def ensemble_distributed(A, B, chains: int, iters: int, schedule, seed: int,
-                         p0_fn: Callable[[int, int], np.ndarray],
+                         p0_fn: Optional[Callable[[int, int], np.ndarray]] = None,
                          local_runner: Optional[Callable] = None,
                          group=None, device=None) -> EnsembleResult:
     """Run `chains` independent chains of `iters` iterations across the ranks of `group`.
 
     p0_fn(begin, count) -> (count, n) int32 start permutations of global chains
-    [begin, begin+count).  local_runner(A, B, begin, p0s, iters, schedule, seed) -> dict with
-    best_cost, best_chain (global id), best_perm, stats{iterations, accepted, near_ties};
-    defaults to qap_ensemble_run on this rank's CUDA device.
+    [begin, begin+count); None = the chain-keyed start permutations (R14b), which
+    qap_ensemble_run generates on the device.  local_runner(A, B, begin, p0s, iters, schedule,
+    seed, count) -> dict with best_cost, best_chain (global id), best_perm,
+    stats{iterations, accepted, near_ties}; defaults to qap_ensemble_run on this rank's device.
     """
     import torch
     import torch.distributed as dist
@@ -58,10 +59,14 @@ def ensemble_distributed(A, B, chains: int, iters: int, schedule, seed: int,
     if local_runner is None:
         local_runner = _gpu_runner(device)
     INT64_MAX = (1 << 63) - 1
+    # Eq.(1) <= sum(A) * max(B) for every permutation: checked identically on every rank before
+    # any work, so no rank can fail alone and leave the others waiting in a collective
+    bound = int(np.asarray(A, np.int64).sum()) * int(np.asarray(B, np.int64).max(initial=0))
+    if bound * chains + chains > INT64_MAX:
+        raise OverflowError("best_cost * chains could overflow the int64 reduction key")
     if end > begin:
-        res = local_runner(A, B, begin, p0_fn(begin, end - begin), iters, schedule, seed)
-        if int(res["best_cost"]) * chains + chains > INT64_MAX:
-            raise OverflowError("best_cost * chains overflows the int64 reduction key")
+        p0s = p0_fn(begin, end - begin) if p0_fn is not None else None
+        res = local_runner(A, B, begin, p0s, iters, schedule, seed, end - begin)
         key0 = int(res["best_cost"]) * chains + int(res["best_chain"])
     else:                                   # more ranks than chains: this rank is idle
         res = dict(best_cost=None, best_chain=-1, best_perm=np.zeros(n, np.int32),
@@ -94,11 +99,13 @@ def ensemble_distributed(A, B, chains: int, iters: int, schedule, seed: int,
 
 
 def _gpu_runner(device):
-    def run(A, B, begin, p0s, iters, schedule, seed):
+    def run(A, B, begin, p0s, iters, schedule, seed, count):
         import torch
         from . import qapsa as Q
         dev = torch.cuda.current_device() if device is None else torch.device(device).index
-        with Q.Solver(A, B, p0s[0], device=dev,
+        n = int(np.asarray(A).shape[0])
+        ctx_p0 = p0s[0] if p0s is not None else np.arange(n, dtype=np.int32)   # not used by the ensemble
+        with Q.Solver(A, B, ctx_p0, device=dev,
                       stream=torch.cuda.current_stream().cuda_stream) as s:
-            return s.ensemble(begin, p0s, iters, schedule, seed)
+            return s.ensemble(begin, p0s, iters, schedule, seed, count=count)
     return run

@@ -12,19 +12,39 @@ import numpy as np
 __all__ = ["read_dat", "write_dat", "read_sln", "write_sln"]
 
 
-def _ints(text: str) -> list[int]:
-    return [int(tok) for tok in text.split()]
+class QaplibError(ValueError):
+    """Malformed QAPLIB file; `kind` is SPEC's error class: "parse" (with the token
+    position), "size" (n < 2) or "domain" (negative entries)."""
+
+    def __init__(self, kind: str, msg: str):
+        super().__init__(f"{kind} error: {msg}")
+        self.kind = kind
+
+
+def _ints(text: str, path: str) -> list[int]:
+    out = []
+    for pos, tok in enumerate(text.split()):
+        try:
+            out.append(int(tok))
+        except ValueError:
+            raise QaplibError("parse", f"{path}: token {pos} ({tok!r}) is not an integer") from None
+    return out
 
 
 def read_dat(path: str):
-    """(A, B) as int32 arrays from a QAPLIB .dat file.  Raises ValueError on a malformed file."""
+    """(A, B) as int32 arrays from a QAPLIB .dat file.  Raises QaplibError (a ValueError) on a
+    malformed file: parse errors with the token position, n < 2, negative entries."""
     with open(path) as f:
-        vals = _ints(f.read())
+        vals = _ints(f.read(), path)
     if not vals:
-        raise ValueError(f"{path}: empty file")
+        raise QaplibError("parse", f"{path}: empty file")
     n = vals[0]
-    if n < 1 or len(vals) != 1 + 2 * n * n:
-        raise ValueError(f"{path}: expected 1 + 2*{n}^2 integers, found {len(vals)}")
+    if n < 2:
+        raise QaplibError("size", f"{path}: n = {n} < 2")
+    if len(vals) != 1 + 2 * n * n:
+        raise QaplibError("parse", f"{path}: expected 1 + 2*{n}^2 integers, found {len(vals)}")
+    if min(vals[1:]) < 0:
+        raise QaplibError("domain", f"{path}: negative entry")
     A = np.array(vals[1:1 + n * n], dtype=np.int64).reshape(n, n)
     B = np.array(vals[1 + n * n:], dtype=np.int64).reshape(n, n)
     if A.min() < np.iinfo(np.int32).min or A.max() > np.iinfo(np.int32).max or \
@@ -50,7 +70,7 @@ def write_dat(path: str, A, B) -> None:
 def read_sln(path: str):
     """(n, cost, p) from a QAPLIB .sln file; p is returned 0-based (int32)."""
     with open(path) as f:
-        vals = _ints(f.read())
+        vals = _ints(f.read(), path)
     if len(vals) < 2:
         raise ValueError(f"{path}: expected n and the cost")
     n, cost = vals[0], vals[1]

@@ -29,10 +29,12 @@ QAP_OPT_RELABEL_CLUSTER = 8
 QAP_OPT_PROPOSAL = 9
 QAP_ENGINE_SHARED_MEMORY, QAP_ENGINE_TENSOR_MEMORY, QAP_ENGINE_RELABEL = 0, 1, 2
 QAP_NEAR_LOG_CAP = 1024
+QAP_ENS_NEAR_LOG_CAP = 65536
 
 # Every symbol include/qapsa.h declares (checked by tests/test_abi.py).
 EXPORTS = ("qap_create", "qap_destroy", "qap_reset", "qap_delta_init", "qap_sa_run", "qap_cost",
            "qap_get_state", "qap_get_near_ties", "qap_schedule_bounds", "qap_ensemble_run",
+           "qap_ensemble_near_ties", "qap_start_perms",
            "qap_set_option", "qap_uses_tensor_core", "qap_engine", "qap_last_kernel_time", "qap_last_scratch_time",
            "qap_status_str",
            "qap_last_error", "qap_version")
@@ -93,6 +95,9 @@ def lib(build_if_missing: bool = True):
                                    C.POINTER(qap_schedule), C.c_uint64, C.POINTER(C.c_int64),
                                    C.POINTER(C.c_uint32), i32p, C.POINTER(qap_stats),
                                    C.POINTER(qap_chain_result)]
+    L.qap_ensemble_near_ties.argtypes = [vp, C.POINTER(C.c_uint32), C.POINTER(C.c_uint64),
+                                         C.POINTER(C.c_uint8), C.c_int32, i32p]
+    L.qap_start_perms.argtypes = [vp, C.c_uint64, C.c_uint32, C.c_uint32, i32p]
     L.qap_set_option.argtypes = [vp, C.c_int32, C.c_int64]
     L.qap_last_kernel_time.argtypes = [vp, C.POINTER(C.c_float), i32p]
     L.qap_last_scratch_time.argtypes = [vp, C.POINTER(C.c_float), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
@@ -211,9 +216,14 @@ def qap_schedule_bounds(ctx):
 
 
 def qap_ensemble_run(ctx, chain_begin, p0s, iters, schedule: qap_schedule, seed,
-                     per_chain: bool = False):
-    p0s, pp = _i32(p0s)
-    count, n = p0s.shape
+                     per_chain: bool = False, count=None, n=None):
+    """p0s: (count, n) start permutations, or None for the device's chain-keyed ones (then
+    count and n are required)."""
+    if p0s is None:
+        pp = None
+    else:
+        p0s, pp = _i32(p0s)
+        count, n = p0s.shape
     best_cost, best_chain = C.c_int64(), C.c_uint32()
     best_perm = np.zeros(n, np.int32)
     st = qap_stats()
@@ -225,6 +235,26 @@ def qap_ensemble_run(ctx, chain_begin, p0s, iters, schedule: qap_schedule, seed,
                stats=st.as_dict())
     if per_chain:
         out["per_chain"] = [{f: getattr(r, f) for f, _ in r._fields_} for r in res]
+    return out
+
+
+def qap_ensemble_near_ties(ctx, cap=QAP_ENS_NEAR_LOG_CAP):
+    """(total flagged, sorted [(chain, k, decision), ...]) of the last qap_ensemble_run."""
+    ch = np.zeros(max(cap, 1), np.uint32)
+    ks = np.zeros(max(cap, 1), np.uint64)
+    ds = np.zeros(max(cap, 1), np.uint8)
+    cnt = C.c_int32()
+    _check(lib().qap_ensemble_near_ties(ctx, ch.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                        ks.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                        ds.ctypes.data_as(C.POINTER(C.c_uint8)), cap, C.byref(cnt)), ctx)
+    m = min(cnt.value, cap)
+    return cnt.value, sorted((int(ch[i]), int(ks[i]), int(ds[i])) for i in range(m))
+
+
+def qap_start_perms(ctx, seed, chain_begin, count, n):
+    """(count, n) chain-keyed start permutations, generated on the device."""
+    out = np.zeros((count, n), np.int32)
+    _check(lib().qap_start_perms(ctx, seed, chain_begin, count, _i32(out)[1]), ctx)
     return out
 
 
@@ -324,8 +354,15 @@ class Solver:
     def engine(self) -> int:
         return qap_engine(self.ctx)
 
-    def ensemble(self, chain_begin, p0s, iters, schedule, seed, per_chain=False):
-        return qap_ensemble_run(self.ctx, chain_begin, p0s, iters, schedule, seed, per_chain)
+    def ensemble(self, chain_begin, p0s, iters, schedule, seed, per_chain=False, count=None):
+        return qap_ensemble_run(self.ctx, chain_begin, p0s, iters, schedule, seed, per_chain,
+                                count=count, n=self.n)
+
+    def ensemble_near_ties(self):
+        return qap_ensemble_near_ties(self.ctx)
+
+    def start_perms(self, seed, chain_begin, count):
+        return qap_start_perms(self.ctx, seed, chain_begin, count, self.n)
 
     def last_kernel_time(self):
         return qap_last_kernel_time(self.ctx)

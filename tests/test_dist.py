@@ -24,7 +24,9 @@ def _free_port():
     return p
 
 
-def oracle_runner(A, B, begin, p0s, iters, sched, seed):
+def oracle_runner(A, B, begin, p0s, iters, sched, seed, count):
+    if p0s is None:                       # chain-keyed start permutations (R14b)
+        p0s = np.stack([O.start_perm(len(A), seed, begin + i) for i in range(count)])
     out = O.ensemble_run(A, B, p0s, begin, iters, sched, seed, threads=2)
     i = int(np.lexsort((np.arange(len(out)), out[:, 1]))[0])
     st = O.Run(A, B, p0s[i], chain=begin + i)
@@ -34,14 +36,14 @@ def oracle_runner(A, B, begin, p0s, iters, sched, seed):
                            near_ties=int(out[:, 3].sum())))
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, keyed=False):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     A, B = taixxa(N, 3)
     sch = O.geometric_schedule_for(A, B, start_perms(N, SEED, 0, 1)[0], ITERS)
     res = ensemble_distributed(A, B, CHAINS, ITERS, sch, SEED,
-                               p0_fn=lambda b, c: start_perms(N, SEED, b, c),
+                               p0_fn=None if keyed else (lambda b, c: start_perms(N, SEED, b, c)),
                                local_runner=oracle_runner, device="cpu")
     q.put((rank, res.best_cost, res.best_chain, res.best_perm.tolist(), res.iterations,
            res.accepted, res.near_ties))
@@ -49,11 +51,11 @@ def _worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
-def _run(world):
+def _run(world, keyed=False):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    ps = [ctx.Process(target=_worker, args=(r, world, port, q, keyed)) for r in range(world)]
     for p in ps:
         p.start()
     out = [q.get(timeout=300) for _ in ps]
@@ -92,3 +94,46 @@ def test_gloo_world3_more_ranks_than_share():
     out2 = _run(2)
     out3 = _run(3)
     assert [o[1:] for o in out2][0] == [o[1:] for o in out3][0]
+
+
+def test_gloo_world2_chain_keyed_start_perms():
+    """p0_fn = None: every rank's chains start from the chain-keyed permutations (R14b), so the
+    result equals one process running all chains from O.start_perm."""
+    A, B = taixxa(N, 3)
+    p0s = np.stack([O.start_perm(N, SEED, c) for c in range(CHAINS)])
+    sch = O.geometric_schedule_for(A, B, start_perms(N, SEED, 0, 1)[0], ITERS)
+    ref = O.ensemble_run(A, B, p0s, 0, ITERS, sch, SEED, threads=2)
+    best = int(np.lexsort((np.arange(CHAINS), ref[:, 1]))[0])
+    out = _run(2, keyed=True)
+    for rank, cost, chain, perm, its, acc, near in out:
+        assert cost == ref[best, 1] and chain == best and O.cost(A, B, perm) == cost
+        assert acc == int(ref[:, 2].sum())
+
+
+def test_overflow_is_rejected_before_any_work():
+    """The reduction-key bound is checked identically on every rank before the local run (so no
+    rank can raise alone and leave the others in a collective)."""
+    A = np.full((4, 4), 60000, np.int64) - np.diag([60000] * 4)
+    called = []
+    with pytest.raises(OverflowError):
+        ensemble_distributed(A, A, 2**40, 10, None, 1, local_runner=lambda *a: called.append(1),
+                             device="cpu")
+    assert not called
+
+
+def test_bench_self_launches_two_ranks_dry_run():
+    """`bench.py --gpus 2` outside torchrun relaunches itself with two ranks (torch.distributed.run,
+    127.0.0.1 rendezvous); --dry-run drives the host path (rank environment, chain partition,
+    the ensemble driver's gloo collectives) without a GPU and rank 0 prints one JSON line."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--dry-run",
+                          "--ens-chains", "9"], capture_output=True, text=True, timeout=300, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["rank0_chains"] == [0, 5] and d["chains"] == 9

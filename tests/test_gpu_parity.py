@@ -3,6 +3,8 @@ same seeded inputs.  Integers (Δ, p, C, counters, digest) must be bit-exact;
 Eq.(2) decisions may differ only at flagged near ties (R16), which the oracle
 then follows.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -64,6 +66,27 @@ def _compare_run(A, B, p0, I, sched: O.Schedule, seed=SA_SEED, opts=(), k_splits
     else:
         np.testing.assert_array_equal(D.astype(np.int64), O.delta_init(A, O.bprime(B, p)))
     return g, tot_acc
+
+
+def _ens_follow(s):
+    """{global chain: [(k, decision), ...]} from the last ensemble's near-tie log (R16)."""
+    cnt, log = s.ensemble_near_ties()
+    assert cnt == len(log)
+    out = {}
+    for c, k, d in log:
+        out.setdefault(c, []).append((k, d))
+    return out
+
+
+def _check_chain(r, A, B, p0, chain, I, sch, seed, follow, proposal=0, mode=O.MODE_DELTA):
+    """One ensemble chain's result against the oracle's single chain with the same global id,
+    following the device's decisions at that chain's flagged near ties (R16)."""
+    o = O.Run(A, B, p0, chain=chain, proposal=proposal, mode=mode).run(0, I, sch, seed,
+                                                                       follow=follow.get(chain))
+    assert (r["cost"], r["best_cost"], r["accepted"], r["near_ties"]) == (
+        o["cost"], o["best_cost"], o["accepted"], o["near_ties"]), chain
+    assert np.uint64(r["digest"]) == np.uint64(o["digest"]), chain
+    assert len(follow.get(chain, [])) == r["near_ties"]
 
 
 # ---------------- a1: Δ-init, Eq.(1), schedule bounds ----------------
@@ -336,12 +359,14 @@ def test_ensemble_per_chain_bit_exact():
     sch = O.geometric_schedule_for(A, B, p0s[0], 30000)
     with Q.Solver(A, B, p0s[0]) as s:
         res = s.ensemble(100, p0s, 30000, _sched(sch), SA_SEED, per_chain=True)
+        follow = _ens_follow(s)
     ref = O.ensemble_run(A, B, p0s, 100, 30000, sch, SA_SEED)
     for i, r in enumerate(res["per_chain"]):
-        if r["near_ties"]:
+        if 100 + i in follow:                   # flagged: replay with the device's decisions
+            _check_chain(r, A, B, p0s[i], 100 + i, 30000, sch, SA_SEED, follow)
             continue
-        assert (r["cost"], r["best_cost"], r["accepted"], r["iterations"]) == tuple(
-            int(x) for x in ref[i, [0, 1, 2, 5]])
+        assert (r["cost"], r["best_cost"], r["accepted"], r["iterations"], r["near_ties"]) == tuple(
+            int(x) for x in ref[i, [0, 1, 2, 5, 3]])
         assert np.uint64(r["digest"]) == np.int64(ref[i, 4]).astype(np.uint64)
     bi = int(np.lexsort((np.arange(50), ref[:, 1]))[0])
     assert res["best_chain"] == 100 + bi and res["best_cost"] == ref[bi, 1]
@@ -371,26 +396,87 @@ def test_config3_full_size():
     _compare_run(A, B, p0, cfg["iters"], sch, mode=O.MODE_SCRATCH)
 
 
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
 @pytest.mark.slow
-def test_config5_full_size_sampled_chains():
-    """BASELINE config 5 (8192 x N=100 x 1e7) on one GPU; sampled chains vs the oracle,
-    argmin consistency and the best permutation's Eq.(1) cost."""
+def test_config5_all_chains_vs_oracle_goldens():
+    """BASELINE config 5 at full size, as bench.py runs it (8192 x N=100 x 1e7 on one GPU, start
+    permutations generated on the device, R14b): EVERY chain's cost, best cost, accepted count,
+    near ties and digest against the oracle's (tests/golden/config5_chains.npz, written by
+    tests/golden/make_goldens.py from oracle/ only).  A chain whose device decision at a flagged
+    near tie differs from the oracle's own is replayed by the oracle following the device (R16).
+    Also the argmin and Eq.(1) of the returned best permutation."""
+    g = np.load(os.path.join(GOLDEN, "config5_chains.npz"))
+    ref, nk, nd = g["out"], g["near_k"], g["near_d"]
+    kind, t0, tf, I = g["schedule"]
     A, B, _, cfg = config(5)
-    C = cfg["chains"]
-    p0s = start_perms(100, SA_SEED, 0, C)
-    sch = O.geometric_schedule_for(A, B, p0s[0], cfg["iters"])
-    with Q.Solver(A, B, p0s[0]) as s:
-        res = s.ensemble(0, p0s, cfg["iters"], _sched(sch), SA_SEED, per_chain=True)
+    n, C = cfg["n"], cfg["chains"]
+    assert (C, int(I)) == (ref.shape[0], cfg["iters"])
+    with Q.Solver(A, B, np.arange(n, dtype=np.int32)) as s:
+        p00 = s.start_perms(SA_SEED, 0, 1)[0]
+        np.testing.assert_array_equal(p00, O.start_perm(n, SA_SEED, 0))
+        s.reset(p00)
+        s.delta_init()
+        assert s.schedule_bounds() == (t0, tf)          # R2 at chain 0's start permutation
+        sch = O.Schedule(int(kind), t0, tf, int(I))
+        res = s.ensemble(0, None, int(I), _sched(sch), SA_SEED, per_chain=True, count=C)
+        follow = _ens_follow(s)
     per = res["per_chain"]
+    got = np.array([[r["cost"], r["best_cost"], r["accepted"], r["near_ties"], r["iterations"]]
+                    for r in per], np.int64)
+    dig = np.array([r["digest"] for r in per], np.uint64)
+    replay = []
+    for c in range(C):
+        m = int(ref[c, 3])
+        oracle_log = [(int(nk[c, i]), int(nd[c, i])) for i in range(min(m, nk.shape[1]))]
+        if follow.get(c, []) != oracle_log:      # a near tie decided differently: replay
+            replay.append(c)
+            continue
+        assert tuple(got[c]) == tuple(int(x) for x in ref[c, [0, 1, 2, 3, 5]]), c
+        assert dig[c] == np.int64(ref[c, 4]).astype(np.uint64), c
+    assert len(replay) <= 8, replay             # near ties are rare (< 1 per 1e8 iterations)
+    for c in replay:
+        _check_chain(per[c], A, B, O.start_perm(n, SA_SEED, c), c, int(I), sch, SA_SEED, follow,
+                     mode=O.MODE_SCRATCH)
     best = min(range(C), key=lambda i: (per[i]["best_cost"], i))
     assert res["best_chain"] == best and res["best_cost"] == per[best]["best_cost"]
     assert O.cost(A, B, res["best_perm"]) == res["best_cost"]
-    for i in [0, 1, 4095, C - 1]:
-        if per[i]["near_ties"]:
-            continue
-        o = O.Run(A, B, p0s[i], mode=O.MODE_SCRATCH, chain=i).run(0, cfg["iters"], sch, SA_SEED)
-        assert (per[i]["cost"], per[i]["best_cost"], per[i]["accepted"], per[i]["digest"]) == (
-            o["cost"], o["best_cost"], o["accepted"], o["digest"])
+    assert int(got[:, 3].sum()) < C * int(I) / 1e8 + 3       # BASELINE: < 1 near tie per 1e8
+
+
+@pytest.mark.slow
+def test_config4_full_run_vs_oracle_goldens():
+    """BASELINE config 4 at full length (N=256 grey density, 1e9 iterations) on the relabel
+    engine (cluster of 8), in ten calls of 1e8: after every call p, best_p, C, best, accepted,
+    digest and the near ties equal the oracle's checkpoints (tests/golden/config4_full.json,
+    written by tests/golden/make_goldens.py from oracle/ only)."""
+    import json
+    with open(os.path.join(GOLDEN, "config4_full.json")) as f:
+        gold = json.load(f)
+    A, B, p0, cfg = config(4)
+    sc = gold["schedule"]
+    sch = O.Schedule(sc["kind"], sc["t0"], sc["tf"], sc["total_iters"])
+    with Q.Solver(A, B, p0) as s:
+        assert s.engine() == Q.QAP_ENGINE_RELABEL
+        s.delta_init()
+        assert s.schedule_bounds() == (sch.t0, sch.tf)
+        k, acc = 0, 0
+        for cp in gold["checkpoints"]:
+            g = s.run(k, cp["k"] - k, _sched(sch), SA_SEED)
+            k = cp["k"]
+            acc += g["accepted"]
+            p, bp, _ = s.state(want_delta=False)
+            n_near, near = s.near_ties()
+            assert near == [tuple(x) for x in cp["near_log"]], k
+            assert (g["cost"], g["best_cost"], acc, n_near) == (
+                cp["cost"], cp["best_cost"], cp["accepted"], cp["near_ties"]), k
+            assert g["digest"] == int(cp["digest"]), k
+            np.testing.assert_array_equal(p, cp["p"])
+            np.testing.assert_array_equal(bp, cp["best_p"])
+        _, _, D = s.state()
+    np.testing.assert_array_equal(D.astype(np.int64), O.delta_init(A, O.bprime(B, p)))
+    assert k == cfg["iters"]
 
 
 def test_qaplib_fixture_through_the_abi():
@@ -432,13 +518,9 @@ def test_random_proposals_ensemble_chains():
     with Q.Solver(A, B, p0s[0]) as s:
         s.set_option(Q.QAP_OPT_PROPOSAL, 1)
         res = s.ensemble(40, p0s, I, _sched(sch), SA_SEED, per_chain=True)
+        follow = _ens_follow(s)
     for i, r in enumerate(res["per_chain"]):
-        ref = O.Run(A, B, p0s[i], chain=40 + i, proposal=1)
-        o = ref.run(0, I, sch, SA_SEED)
-        if r["near_ties"] or o["near_ties"]:
-            continue
-        assert (r["cost"], r["best_cost"], r["accepted"]) == (o["cost"], o["best_cost"], o["accepted"])
-        assert np.uint64(r["digest"]) == np.uint64(o["digest"])
+        _check_chain(r, A, B, p0s[i], 40 + i, I, sch, SA_SEED, follow, proposal=1)
 
 
 @pytest.mark.parametrize("engine", [pytest.param([(RLB, 3)], id="relabel"),
@@ -470,17 +552,148 @@ def test_ensemble_tensor_memory_vs_shared_memory():
     C, I = 40, 50000
     p0s = start_perms(60, SA_SEED, 7, C)
     sch = O.geometric_schedule_for(A, B, p0s[0], I)
-    out = {}
+    out, fol = {}, {}
     for tcv in (1, 0):
         with Q.Solver(A, B, p0s[0]) as s:
             s.set_option(TC, tcv)
             out[tcv] = s.ensemble(7, p0s, I, _sched(sch), SA_SEED, per_chain=True)
+            fol[tcv] = _ens_follow(s)
     assert out[1]["best_cost"] == out[0]["best_cost"] and out[1]["best_chain"] == out[0]["best_chain"]
     np.testing.assert_array_equal(out[1]["best_perm"], out[0]["best_perm"])
+    assert fol[1] == fol[0]
     for i, (r1, r0) in enumerate(zip(out[1]["per_chain"], out[0]["per_chain"])):
         assert r1 == r0, i
-        if i < 6:
-            o = O.Run(A, B, p0s[i], chain=7 + i).run(0, I, sch, SA_SEED)
-            if not o["near_ties"]:
-                assert (r1["cost"], r1["best_cost"], r1["accepted"]) == (o["cost"], o["best_cost"], o["accepted"])
-                assert np.uint64(r1["digest"]) == np.uint64(o["digest"])
+        if i < 6 or 7 + i in fol[1]:
+            _check_chain(r1, A, B, p0s[i], 7 + i, I, sch, SA_SEED, fol[1])
+
+
+# ---------------- R16: constructed near ties through every engine ----------------
+
+def _near_tie_setup(n=12, inst=3, seed=SA_SEED, chain=0, I=5000):
+    """Instance, p0 and a constant schedule T = δ/(-ln r_0) that make iteration 0 (pair (0,1),
+    δ = Δ_01(p0) > 0) a near tie for `chain` (R16)."""
+    import math
+    A, B = taixxa(n, inst)
+    for c in range(64):
+        p0 = start_perm(n, inst, c)
+        d = int(O.delta_init(A, O.bprime(B, p0))[0])
+        if d > 0:
+            break
+    T = d / -math.log(O.uniform(seed, 0, chain, 0))
+    return A, B, p0, O.Schedule(O.COOL_GEOMETRIC, T, T, I)
+
+
+NEAR_ENGINES = ENGINES + [pytest.param([(TC, 0), (RLB, 3)], id="relabel"),
+                          pytest.param([(TC, 0), (RLB, 3), (RLBC, 1)], id="relabel_1sm")]
+
+
+@pytest.mark.parametrize("engine", NEAR_ENGINES)
+def test_constructed_near_tie_single_chain(engine):
+    """A flagged near tie at k = 0 on every single-chain engine: the device flags it, logs its
+    decision, and the oracle following that decision reproduces the whole run bit-exactly."""
+    A, B, p0, sch = _near_tie_setup()
+    with Q.Solver(A, B, p0) as s:
+        for kv in engine:
+            s.set_option(*kv)
+        if engine[-1] == (RLB, 3) or engine[-1] == (RLBC, 1):
+            assert s.engine() == Q.QAP_ENGINE_RELABEL
+    g, _ = _compare_run(A, B, p0, sch.total_iters, sch, opts=engine)
+    with Q.Solver(A, B, p0) as s:
+        for kv in engine:
+            s.set_option(*kv)
+        s.delta_init()
+        s.run(0, sch.total_iters, _sched(sch), SA_SEED)
+        n_near, near = s.near_ties()
+    assert n_near >= 1 and near[0][0] == 0
+
+
+@pytest.mark.parametrize("tc", [1, 0])
+def test_constructed_near_tie_ensemble_chain(tc):
+    """An ensemble in which chain 5 (global id) has a near tie at k = 0: the device logs (5, 0,
+    decision) in the ensemble near-tie log, and the oracle's single chain 5 following it matches;
+    every other chain matches the oracle too (tensor-memory and shared-memory ensembles)."""
+    C, I = 8, 4000
+    A, B, _, _ = _near_tie_setup()
+    import math
+    p0s = start_perms(12, 3, 0, C)
+    d = int(O.delta_init(A, O.bprime(B, p0s[5]))[0])
+    if d <= 0:
+        p0s[5] = p0s[5][[1, 0] + list(range(2, 12))]
+        d = int(O.delta_init(A, O.bprime(B, p0s[5]))[0])
+    assert d > 0
+    T = d / -math.log(O.uniform(SA_SEED, 0, 5, 0))
+    sch = O.Schedule(O.COOL_GEOMETRIC, T, T, I)
+    with Q.Solver(A, B, p0s[0]) as s:
+        s.set_option(TC, tc)
+        res = s.ensemble(0, p0s, I, _sched(sch), SA_SEED, per_chain=True)
+        follow = _ens_follow(s)
+    assert 5 in follow and follow[5][0][0] == 0
+    for i, r in enumerate(res["per_chain"]):
+        _check_chain(r, A, B, p0s[i], i, I, sch, SA_SEED, follow)
+
+
+# ---------------- R14b: chain-keyed start permutations on the device ----------------
+
+@pytest.mark.parametrize("n", [2, 3, 12, 100, 256])
+def test_start_perms_match_oracle(n):
+    A, B = taixxa(n, 1)
+    with Q.Solver(A, B, np.arange(n, dtype=np.int32)) as s:
+        got = s.start_perms(SA_SEED, 1000, 17)
+    for i in range(17):
+        np.testing.assert_array_equal(got[i], O.start_perm(n, SA_SEED, 1000 + i))
+
+
+@pytest.mark.parametrize("tc", [1, 0])
+def test_ensemble_device_start_perms(tc):
+    """qap_ensemble_run with p0s = NULL: chains start from the device's chain-keyed permutations
+    and equal the oracle's chains started from O.start_perm (no host start array)."""
+    A, B = taixxa(30, 9)
+    C, I = 20, 30000
+    sch = O.geometric_schedule_for(A, B, O.start_perm(30, SA_SEED, 0), I)
+    with Q.Solver(A, B, np.arange(30, dtype=np.int32)) as s:
+        s.set_option(TC, tc)
+        res = s.ensemble(300, None, I, _sched(sch), SA_SEED, per_chain=True, count=C)
+        follow = _ens_follow(s)
+    p0s = np.stack([O.start_perm(30, SA_SEED, 300 + i) for i in range(C)])
+    ref = O.ensemble_run(A, B, p0s, 300, I, sch, SA_SEED)
+    for i, r in enumerate(res["per_chain"]):
+        if 300 + i in follow:
+            _check_chain(r, A, B, p0s[i], 300 + i, I, sch, SA_SEED, follow)
+            continue
+        assert (r["cost"], r["best_cost"], r["accepted"]) == tuple(int(x) for x in ref[i, :3])
+    bi = int(np.lexsort((np.arange(C), ref[:, 1]))[0])
+    assert res["best_chain"] == 300 + bi
+
+
+@pytest.mark.parametrize("n", [127, 128])
+def test_tmem_ensemble_at_the_lane_limit(n):
+    """Tensor-memory ensemble at N = 127, 128 (H columns of the last window rows stay inside a
+    chain's 256 TMEM columns; two chains per SM)."""
+    rng = np.random.default_rng(n)
+    A = np.triu(rng.integers(0, 128, size=(n, n)), 1).astype(np.int32)
+    B = np.triu(rng.integers(0, 128, size=(n, n)), 1).astype(np.int32)
+    A, B = A + A.T, B + B.T
+    C, I = 6, 40000
+    p0s = start_perms(n, 2, 0, C)
+    sch = O.geometric_schedule_for(A, B, p0s[0], I)
+    with Q.Solver(A, B, p0s[0]) as s:
+        assert s.uses_tensor_core()
+        res = s.ensemble(0, p0s, I, _sched(sch), SA_SEED, per_chain=True)
+        follow = _ens_follow(s)
+    for i, r in enumerate(res["per_chain"]):
+        _check_chain(r, A, B, p0s[i], i, I, sch, SA_SEED, follow)
+
+
+def test_tmem_ensemble_more_chains_than_grid_y():
+    """65537 chains (more than gridDim.y allows in one Δ-rebuild launch): every sampled chain
+    equals the oracle's."""
+    A, B = taixxa(8, 8)
+    C, I = 65537, 300
+    sch = O.geometric_schedule_for(A, B, O.start_perm(8, SA_SEED, 0), I)
+    with Q.Solver(A, B, np.arange(8, dtype=np.int32)) as s:
+        assert s.uses_tensor_core()
+        res = s.ensemble(0, None, I, _sched(sch), SA_SEED, per_chain=True, count=C)
+        follow = _ens_follow(s)
+    per = res["per_chain"]
+    for c in [0, 1, 65534, 65535, 65536]:
+        _check_chain(per[c], A, B, O.start_perm(8, SA_SEED, c), c, I, sch, SA_SEED, follow)

@@ -109,16 +109,39 @@ def test_seed_and_chain_change_trajectory():
     assert a["digest"] != b["digest"] and a["digest"] != c["digest"]
 
 
-def test_follow_mode_overrides_only_listed_near_ties():
-    """R16: follow entries are adopted only at near ties; other k are ignored."""
+def near_tie_schedule(A, B, p0, seed, chain=0, I=5000):
+    """A constant schedule (t0 = tf = T) that makes iteration 0 a near tie (R16): iteration 0
+    proposes pair (0, 1) (R4) with δ = Δ_01 at p0 > 0, and T = δ / (-ln r_0) puts
+    δ + T ln r_0 within rounding of 0."""
+    import math
+    d = int(O.delta_init(A, O.bprime(B, p0))[0])
+    assert d > 0
+    T = d / -math.log(O.uniform(seed, 0, chain, 0))
+    return O.Schedule(O.COOL_GEOMETRIC, T, T, I)
+
+
+def test_constructed_near_tie_is_flagged_and_followed():
+    """R16 on a constructed near tie: the oracle flags iteration 0 (and only it, at the start),
+    logs its own decision, adopts a listed decision at a flagged k in either direction, and
+    ignores listed decisions at k that are not near ties."""
     A, B = taixxa(12, 3)
-    p0 = start_perm(12, 3, 0)
-    sch = _sched(A, B, p0, 5000)
-    base = O.Run(A, B, p0).run(0, 5000, sch, seed=3)
-    bogus = [(k, 1) for k in range(0, 5000, 7)]
+    for c in range(40):
+        p0 = start_perm(12, 3, c)
+        if O.delta_init(A, O.bprime(B, p0))[0] > 0:
+            break
+    sch = near_tie_schedule(A, B, p0, seed=3)
+    one = O.Run(A, B, p0)
+    st = one.run(0, 1, sch, seed=3)
+    assert st["near_ties"] == 1 and one.near_log == [(0, st["accepted"])]
+    for d in (0, 1):                              # the follow entry decides iteration 0
+        r = O.Run(A, B, p0)
+        assert r.run(0, 1, sch, seed=3, follow=[(0, d)])["accepted"] == d
+        assert r.near_log == [(0, d)]
+    base = O.Run(A, B, p0)
+    b = base.run(0, 5000, sch, seed=3)
+    bogus = [(k, 1 - (k % 2)) for k in range(1, 5000, 7) if k not in [x for x, _ in base.near_log]]
     other = O.Run(A, B, p0).run(0, 5000, sch, seed=3, follow=bogus)
-    if base["near_ties"] == 0:
-        assert other == base
+    assert other == b
 
 
 def test_all_zero_flow_accepts_everything():

@@ -47,3 +47,17 @@ def test_malformed_files_raise(tmp_path):
     g.write_text("3 10\n1 1 2\n")
     with pytest.raises(ValueError):
         qaplib.read_sln(str(g))
+
+
+@pytest.mark.parametrize("text,kind", [("1\n0\n0\n", "size"), ("2\n0 -1 -1 0\n0 1 1 0\n", "domain"),
+                                       ("2\n0 1 1 x\n0 1 1 0\n", "parse")])
+def test_spec_error_kinds(tmp_path, text, kind):
+    """SPEC's error classes: n < 2 is a size error, negative entries a domain error, a bad token
+    a parse error that names its position."""
+    f = tmp_path / "e.dat"
+    f.write_text(text)
+    with pytest.raises(qaplib.QaplibError) as ei:
+        qaplib.read_dat(str(f))
+    assert ei.value.kind == kind
+    if kind == "parse":
+        assert "token 4" in str(ei.value)
