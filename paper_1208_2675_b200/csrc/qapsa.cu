@@ -72,6 +72,9 @@ struct qap_ctx {
     uint8_t* dcls = nullptr;            // n
     uint16_t* dpt = nullptr;            // ncls x (n+1)
     int32_t* dD2 = nullptr;             // quad layout, same size as dD
+    // thresholds θ of a single-chain call's iterations (k_theta, theta_ring.cuh), grown on demand
+    float* dtheta = nullptr;
+    size_t theta_cap = 0;
     // near-tie log of the last qap_ensemble_run: (chain, k, decision), R16
     unsigned int* ens_near_count = nullptr;
     unsigned long long* ens_near_k = nullptr;
@@ -266,7 +269,7 @@ void qap_destroy(qap_ctx* c) {
                     c->dnear_k, c->dnear_dec, c->dscratch, c->ens_p0, c->ens_res, c->ens_best,
                     c->ens_counter, c->dkout, c->dcls, c->dpt, c->dD2, c->tp, c->tbp, c->tD,
                     c->tst, c->tkout, c->ens_near_count, c->ens_near_k, c->ens_near_dec,
-                    c->ens_near_chain};
+                    c->ens_near_chain, c->dtheta};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->ev0) cudaEventDestroy(c->ev0);
@@ -542,6 +545,18 @@ qap_status qap_sa_run(qap_ctx* c, uint64_t k0, uint64_t iters, const qap_schedul
     a.n = c->n; a.ld = c->ld; a.M = c->M; a.wmax = std::min(c->wmax, threads);
     a.k0 = k0; a.k_end = k0 + iters; a.seed = seed; a.sch = sch;
 
+    a.theta = nullptr;
+    a.theta_kb = a.theta_cnt = 0;
+    if (tc) {   // θ buffer of one chunk of the call (theta_ring.cuh)
+        const size_t need = (size_t)((std::min<uint64_t>(iters, TH_CHUNK) + TH_BLK - 1) / TH_BLK) * TH_BLK;
+        if (c->theta_cap < need) {
+            if (c->dtheta) cudaFree(c->dtheta);
+            c->dtheta = nullptr;
+            c->theta_cap = 0;
+            if (cudaMalloc(&c->dtheta, need * 4) != cudaSuccess) return fail(c, QAP_E_NOMEM, "θ buffer");
+            c->theta_cap = need;
+        }
+    }
     CU(cudaEventRecord(c->ev0, c->stream));
     a.k0_dev = nullptr;
     a.proposal = c->proposal;
@@ -549,29 +564,52 @@ qap_status qap_sa_run(qap_ctx* c, uint64_t k0, uint64_t iters, const qap_schedul
     a.dstride = 0;
     a.chain = 0u;
     a.switch_gap = 0;
+    int launches = 0;
     if (tc) {
         a.wmax = c->wmax;
         // compile-time problem size for the BASELINE configurations, generic otherwise
         auto kern = c->n == 100 ? k_sa_tc<100> : c->n == 50 ? k_sa_tc<50> : c->n == 12 ? k_sa_tc<12> : k_sa_tc<0>;
         CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        if (c->use_scratch) {
-            // f2: the high-acceptance phase without Δ, then Δ rebuilt at the iteration reached and
-            // the Δ engine from there (device-side chaining, no host round trip)
-            auto ks = c->n == 100 ? k_sa_scratch<100> : c->n == 50 ? k_sa_scratch<50>
-                    : c->n == 12 ? k_sa_scratch<12> : k_sa_scratch<0>;
-            const int ssm = sc_layout(c->ld).bytes;
-            CU(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, ssm));
-            ks<<<1, TCS_NT, ssm, c->stream>>>(a, c->dkout);
+        auto ks = c->n == 100 ? k_sa_scratch<100> : c->n == 50 ? k_sa_scratch<50>
+                : c->n == 12 ? k_sa_scratch<12> : k_sa_scratch<0>;
+        const int ssm = sc_layout(c->ld).bytes;
+        CU(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, ssm));
+        bool scratch = c->use_scratch != 0;
+        // chunks of TH_CHUNK iterations: θ of the chunk on the whole GPU, then the chain kernels
+        for (uint64_t kc = k0; kc < k0 + iters; kc += TH_CHUNK) {
+            const uint64_t ke = std::min<uint64_t>(k0 + iters, kc + TH_CHUNK);
+            const uint64_t cnt = (ke - kc + TH_BLK - 1) / TH_BLK * TH_BLK;
+            k_theta<<<c->num_sms * 4, 256, 0, c->stream>>>(sch, seed, 0u, kc, cnt, c->dtheta);
             CU(cudaGetLastError());
-            CU(cudaEventRecord(c->evm, c->stream));
-            const int dt = 256, db = (c->M + dt - 1) / dt;
-            k_delta_init<uint8_t, uint8_t><<<db, dt, 0, c->stream>>>((const uint8_t*)c->dA, (const uint8_t*)c->dB,
-                                                                     c->dp, c->drowaddr, c->n, c->ld, c->M, c->dD);
+            a.k0 = kc;
+            a.k_end = ke;
+            a.theta = c->dtheta;
+            a.theta_kb = kc;
+            a.theta_cnt = cnt;
+            a.k0_dev = nullptr;
+            launches += 2;
+            if (scratch) {
+                // f2: the high-acceptance phase without Δ, then Δ rebuilt at the iteration reached and
+                // the Δ engine from there (device-side chaining, no host round trip)
+                ks<<<1, TCS_NT, ssm, c->stream>>>(a, c->dkout);
+                CU(cudaGetLastError());
+                if (kc == k0) CU(cudaEventRecord(c->evm, c->stream));
+                const int dt = 256, db = (c->M + dt - 1) / dt;
+                k_delta_init<uint8_t, uint8_t><<<db, dt, 0, c->stream>>>((const uint8_t*)c->dA, (const uint8_t*)c->dB,
+                                                                         c->dp, c->drowaddr, c->n, c->ld, c->M, c->dD);
+                CU(cudaGetLastError());
+                a.k0_dev = c->dkout;
+                launches += 2;
+            }
+            kern<<<1, TCK_NT, smem, c->stream>>>(a);
             CU(cudaGetLastError());
-            a.k0_dev = c->dkout;
+            if (scratch && ke < k0 + iters) {    // did the scratch phase end inside this chunk?
+                unsigned long long kr = 0;
+                CU(cudaMemcpyAsync(&kr, c->dkout, sizeof kr, cudaMemcpyDeviceToHost, c->stream));
+                CU(cudaStreamSynchronize(c->stream));
+                scratch = kr >= ke;
+            }
         }
-        kern<<<1, TCK_NT, smem, c->stream>>>(a);
-        CU(cudaGetLastError());
     } else if (rlb) {
         RelabelArgs ra;
         ra.c = a;
@@ -614,7 +652,7 @@ qap_status qap_sa_run(qap_ctx* c, uint64_t k0, uint64_t iters, const qap_schedul
         CU(cudaEventElapsedTime(&c->last_scratch_ms, c->ev0, c->evm));
         CU(cudaMemcpy(c->last_scratch, c->dkout, sizeof c->last_scratch, cudaMemcpyDeviceToHost));
     }
-    c->last_launches = (tc && c->use_scratch) ? 3 : 1;
+    c->last_launches = tc ? launches : 1;
     if (out) {
         out->iterations = iters;
         out->accepted = after.accepted - before.accepted;
@@ -779,6 +817,7 @@ static qap_status ensemble_tc(qap_ctx* c, uint32_t chain_begin, uint32_t chain_c
     a.k0 = 0; a.k_end = iters; a.seed = seed; a.sch = sch;
     a.k0_dev = nullptr; a.proposal = 0;
     a.ens = 1; a.dstride = dstride; a.chain = chain_begin;
+    a.theta = nullptr; a.theta_kb = a.theta_cnt = 0;
     // two scratch-phase chains share an SM but the Δ engine holds one: stay longer in the scratch
     // phase (config 5: gap 4096 / 16384 / 65536 / never = 3.67 / 3.64 / 3.62 / 3.66 s)
     a.switch_gap = 65536;

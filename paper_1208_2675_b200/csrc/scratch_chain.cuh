@@ -25,6 +25,7 @@
 #include <cstdint>
 
 #include "tc_chain.cuh"
+#include "theta_ring.cuh"
 
 namespace qapsa {
 
@@ -38,7 +39,7 @@ template <bool ENS> __host__ __device__ constexpr uint32_t tcs_cols() { return E
 constexpr uint64_t TCS_SWITCH_GAP = 4096;   // switch to the Δ engine after this many iterations without an accept
 
 struct ScLayout {
-    int a, b, rg, la, tmp, p, bestp, dg, xch, slots, rec, thm, misc, bytes;
+    int a, b, rg, la, tmp, p, bestp, dg, xch, slots, rec, misc, tbar, bytes;
 };
 __host__ __device__ inline ScLayout sc_layout(int ld) {
     ScLayout L;
@@ -48,21 +49,22 @@ __host__ __device__ inline ScLayout sc_layout(int ld) {
     o = (o + 1023) & ~1023;
     L.rg = o;    o += 256 * 32;                 // [G | H] update B operand, K-major canonical (SBO 256)
     L.la = o;    o += 128 * 32;                 // its A operand [dA, -dBf], same layout
-    L.tmp = o;   o += 2 * 128 * 128;            // init only: A, C canonical (SBO 1024)
+    L.tmp = o;   o += 2 * 128 * 128;            // init: A, C canonical (SBO 1024); then the θ ring
     L.p = o;     o += 128 * 2;
     L.bestp = o; o += 128 * 2;
     L.dg = o;    o += 128 * 4;                  // D_x
     L.xch = o;   o += 4 * 128 * 4;              // G[u_i][p(v)] by window row i and location v
     L.slots = o; o += 2 * 4 * 16;
-    L.rec = o;   o += 32;
-    L.thm = o;   o += TCK_TH * 8;
+    L.rec = o;   o += 32;                       // the accept for the helpers, double-buffered
     L.misc = o;  o += 64;                       // mbarrier | TMEM base
+    L.tbar = o;  o += TH_SLOTS * 8;             // θ ring mbarriers
     L.bytes = o;
     return L;
 }
 
 template <int NFIX, bool ENS = false>
 __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, unsigned long long* k_out) {
+    constexpr bool RING = !ENS;                  // single chain: precomputed θ (theta_ring.cuh)
     extern __shared__ __align__(16) unsigned char smem[];
     const ChainView cv = chain_view<ENS>(a);     // this CTA's chain (ensemble launches)
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -80,10 +82,8 @@ __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, uns
     int* xch = reinterpret_cast<int*>(smem + L.xch);
     int4* slots = reinterpret_cast<int4*>(smem + L.slots);
     int* rec = reinterpret_cast<int*>(smem + L.rec);
-    float2* thm = reinterpret_cast<float2*>(smem + L.thm);
     uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + L.misc);          // G|H update done
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.misc + 8);
-    uint64_t* mbar_t = reinterpret_cast<uint64_t*>(smem + L.misc + 16);   // next-window thresholds written
     const bool lanew = warp < 4;
     const uint32_t quad_lane = (uint32_t)(32 * (warp & 3)) << 16;
     const int v = t & 127;
@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, uns
     }
     for (int i = t; i < (256 + 128) * 32 / 16; i += TCS_NT) reinterpret_cast<uint4*>(Rg)[i] = make_uint4(0, 0, 0, 0);
     if (warp == 0) tc::tmem_alloc(tmem_slot, tcs_cols<ENS>());
-    if (t == 0) { tc::mbar_init(mbar, 1); tc::mbar_init(mbar_t, 4); }
+    if (t == 0) tc::mbar_init(mbar, 1);
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
@@ -144,6 +144,10 @@ __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, uns
     tc::mbar_wait(mbar, 0);
     uint32_t ph = 1;
     tc::fence_after_sync();
+    // single chain: θ of the window from the precomputed ring (reuses the init operands' space)
+    ThetaRing TR = theta_ring(reinterpret_cast<float*>(smem + L.tmp), reinterpret_cast<uint64_t*>(smem + L.tbar),
+                              a.theta, a.theta_kb, a.theta_cnt, a.k0);
+    if (RING && t == 0 && a.k0 < a.k_end) TR.start(a.k0);
     __syncthreads();
 
     const Sched sch = a.sch;
@@ -158,16 +162,23 @@ __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, uns
     int W = wmax;
     int parity = 0;
     int rejI = rej_bound(sch, k);
-    uint64_t pk = ~0ull;                         // window whose thresholds are in thm
-    int pn = 0;
+    float Tw = temp32(sch, k);                   // T at the window's first iteration (ring margin)
     const uint32_t id_gh = tc::idesc_i8(128, 256, true);
 #ifdef QAPSA_PHASE_TIMERS
     long long tacc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 #endif
 
   if (lanew) {
-    uint32_t ph_t = 0;                           // phase of the thresholds mbarrier (one per accept)
     const uint64_t gap = a.switch_gap ? a.switch_gap : TCS_SWITCH_GAP;
+    // The window's rows u_i = u0 + i: pu[i] = p(u_i), gv[i] = G[v][p(u_i)] (registers) and
+    // xch[i][v] = G_{u_i, v} (shared memory).  After an accept they are produced by the stage from
+    // the PRE-update tensor memory plus the exact rank-1 change of the accept, so the next window
+    // is tested while the tensor cores apply that change (the MMA is waited for only before the
+    // next read or write of tensor memory); after a window without accept they are read afresh.
+    bool fresh = true;
+    bool mma_pending = false;
+    int pu[4];
+    uint32_t gv[4];
     while (k < k_end && k - k_last < gap) {
         // ---------------- window: rows u0 .. u0+R-1 (R <= 4) ----------------
         TCT_MARK(pt0, u0 + v0);
@@ -178,7 +189,11 @@ __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, uns
             const uint64_t remaining = k_end - k;
             if ((uint64_t)Wl > remaining) Wl = (int)remaining;
         }
-        int rb[4], rf[4], pu[4];
+        if (RING) {
+            if (t == 0) TR.refill(k);
+            TR.ensure(k + (uint64_t)Wl);
+        }
+        int rb[4], rf[4];
         {
             int f = 0;
 #pragma unroll
@@ -186,28 +201,36 @@ __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, uns
                 rf[i] = i == 0 ? v0 : u0 + i + 1;
                 rb[i] = f - rf[i];
                 f += i == 0 ? L0 : m1 - i;
-                pu[i] = p[min(u0 + i, n - 1)];
             }
         }
-        uint32_t gv[4], hf[4];                   // G[v][p(u_i)] (location lane v), H[f][u_i] (facility lane f = v)
+        if (fresh) {
+            if (mma_pending) {                   // G, H complete before they are read
+                tc::mbar_wait(mbar, ph);
+                ph ^= 1;
+                tc::fence_after_sync();
+                mma_pending = false;
+            }
+            uint32_t hf[4];                      // H[f][u_i] (facility lane f = v)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) tc::tmem_ld1(tm + quad_lane + TCS_COL_G + (uint32_t)pu[i], gv[i]);
-        // H columns u0 .. u0+3 must stay inside [TCS_COL_H, TCS_COL_H + 128) (an ensemble CTA owns
-        // only 256 columns): read from hb = min(u0, 124) and shift (rows past n-1 are never used)
-        const int hb = min(u0, 124), hsh = u0 - hb;
-        tc::tmem_ld4(tm + quad_lane + TCS_COL_H + (uint32_t)hb, hf);
-        tc::tmem_wait_ld();
-        if (hsh) {                               // warp-uniform, only in the last rows of the triangle
+            for (int i = 0; i < 4; ++i) pu[i] = p[min(u0 + i, n - 1)];
 #pragma unroll
-            for (int i = 0; i < 3; ++i) hf[i] = hsh == 1 ? hf[i + 1] : (i < 2 ? hf[i + 2] : hf[3]);
+            for (int i = 0; i < 4; ++i) tc::tmem_ld1(tm + quad_lane + TCS_COL_G + (uint32_t)pu[i], gv[i]);
+            // H columns u0 .. u0+3 must stay inside [TCS_COL_H, TCS_COL_H + 128) (an ensemble CTA owns
+            // only 256 columns): read from hb = min(u0, 124) and shift (rows past n-1 are never used)
+            const int hb = min(u0, 124), hsh = u0 - hb;
+            tc::tmem_ld4(tm + quad_lane + TCS_COL_H + (uint32_t)hb, hf);
+            tc::tmem_wait_ld();
+            if (hsh) {                           // warp-uniform, only in the last rows of the triangle
+#pragma unroll
+                for (int i = 0; i < 3; ++i) hf[i] = hsh == 1 ? hf[i + 1] : (i < 2 ? hf[i + 2] : hf[3]);
+            }
+            if (vin) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) xch[i * 128 + qv] = (int)hf[i];   // G[u_i][v] to location p^-1(v)
+            }
+            group_sync(3, 128);                  // exchange
         }
-        if (vin) {
-#pragma unroll
-            for (int i = 0; i < 4; ++i) xch[i * 128 + qv] = (int)hf[i];   // G[u_i][v] to location p^-1(v)
-        }
-        TCT_ACC(0, pt0, u0);
-        group_sync(3, 128);                      // exchange
-        TCT_ACC(1, pt0, xch[v]);
+        TCT_ACC(0, pt0, xch[v]);
         int4* sl = slots + parity * 4;
         unsigned acc_mask = 0, near_mask = 0;
         const int dv = Dg[v];
@@ -224,17 +247,35 @@ __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, uns
             acc_mask |= (unsigned)(ex && dd[i] <= 0) << i;      // δ <= 0 (R5)
             need |= (unsigned)(ex && dd[i] > 0 && dd[i] <= rejI) << i;
         }
-        const bool prepared = pk == k;           // the first window after an accept
-        if (__any_sync(0xffffffffu, need != 0)) {
-            const int pnk = prepared ? pn : 0;
-            if (prepared) tc::mbar_wait(mbar_t, ph_t);   // the helpers' thresholds are written
+        if (RING) {                              // branch-free θ test; the exact path only inside the margin
+            unsigned band = 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int o = rb[i] + v;
+                const float th = TR.at(k + (uint64_t)max(o, 0));
+                const float m = 2e-4f * th + 2e-5f * Tw;
+                const float df = (float)dd[i];
+                const bool nd = (need >> i) & 1u;
+                acc_mask |= (unsigned)(nd && df < th - m) << i;
+                band |= (unsigned)(nd && !(df < th - m) && !(df > th + m)) << i;
+            }
+            if (__any_sync(0xffffffffu, band != 0)) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    if ((band >> i) & 1u) {      // inside the margin: exact double test (R16)
+                        const int x = tc_exact(dd[i], k + (uint64_t)(rb[i] + v), sch, seed, cv.chain);
+                        acc_mask |= (unsigned)(x & 1) << i;
+                        near_mask |= (unsigned)((x >> 1) & 1) << i;
+                    }
+                }
+            }
+        } else if (__any_sync(0xffffffffu, need != 0)) {
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 if ((need >> i) & 1u) {
                     const int o = rb[i] + v;
                     float th, m;
-                    if (o < pnk) { const float2 q = thm[o]; th = q.x; m = q.y; }
-                    else theta_of(sch, seed, cv.chain, k + (uint64_t)o, &th, &m);
+                    theta_of(sch, seed, cv.chain, k + (uint64_t)o, &th, &m);
                     const float df = (float)dd[i];
                     bool ac = df < th - m;
                     if (!ac && !(df > th + m)) {  // inside the margin: exact double test (R16)
@@ -246,7 +287,6 @@ __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, uns
                 }
             }
         }
-        if (prepared) ph_t ^= 1;                 // one thresholds phase per accept
         int best_o = INT_MAX, best_d = 0, best_rs = 0;
 #pragma unroll
         for (int i = 3; i >= 0; --i) {
@@ -259,7 +299,7 @@ __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, uns
             const int wmin = __reduce_min_sync(0xffffffffu, best_o);
             if (best_o == wmin && (wmin != INT_MAX || lane == 0)) sl[warp] = make_int4(best_o, best_d, best_rs, 0);
         }
-        TCT_ACC(2, pt0, acc_mask);
+        TCT_ACC(1, pt0, acc_mask);
         group_sync(4, 128);                      // window decision
         const int tv = lane < 4 ? sl[lane].x : INT_MAX;
         const int j = __reduce_min_sync(0xffffffffu, tv);
@@ -276,10 +316,13 @@ __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, uns
             }
         }
         if (j == INT_MAX) {
+            TCT_ACC(4, pt0, j);
             k += (uint64_t)Wl;
             win_advance<4>(n, u0, v0, Wl, &u0, &v0);
             W = min(2 * W, wmax);
             rejI = rej_bound(sch, k);
+            Tw = temp32(sch, k);
+            fresh = true;
             continue;
         }
         const unsigned bw = __ballot_sync(0xffffffffu, tv == j);
@@ -288,7 +331,27 @@ __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, uns
         const int r = win.z & 0xFF, s = (win.z >> 8) & 0xFF;
         const int pr = (win.z >> 16) & 0xFF, ps = (int)((unsigned)win.z >> 24);
         const uint64_t kacc = k + (uint64_t)j;
-        // ---------------- stage: the G|H update operands, D'' ----------------
+        // ---------------- stage: the G|H update operands, D'', the next window's rows ----------------
+        int nu0, nv0;                            // next window: cursor after (r, s)
+        next_pair(n, r, s, &nu0, &nv0);
+        int npu[4];                              // facilities of the next window's rows after the swap
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int u = min(nu0 + i, n - 1);
+            npu[i] = u == r ? ps : u == s ? pr : (int)p[u];
+        }
+        if (mma_pending) {                       // the previous update complete: tensor memory is current
+            tc::mbar_wait(mbar, ph);
+            ph ^= 1;
+            tc::fence_after_sync();
+        }
+        uint32_t gps, gpr, g4[4], h4[4];         // PRE-update tensor memory
+        tc::tmem_ld1(tm + quad_lane + TCS_COL_G + (uint32_t)ps, gps);   // G[v][p(s)]
+        tc::tmem_ld1(tm + quad_lane + TCS_COL_G + (uint32_t)pr, gpr);   // G[v][p(r)]
+#pragma unroll
+        for (int i = 0; i < 4; ++i) tc::tmem_ld1(tm + quad_lane + TCS_COL_G + (uint32_t)npu[i], g4[i]);
+        const int hb = min(nu0, 124), hsh = nu0 - hb;
+        tc::tmem_ld4(tm + quad_lane + TCS_COL_H + (uint32_t)hb, h4);
         int arv = 0, asv = 0, brv = 0, bsv = 0, bfr = 0, bfs = 0;
         if (vin) {
             arv = As[r * ld + v]; asv = As[s * ld + v];
@@ -296,36 +359,81 @@ __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, uns
             bfr = Bs[pr * ld + v]; bfs = Bs[ps * ld + v];
         }
         const int dA = arv - asv, dB = brv - bsv, dBf = bfr - bfs;
-        uint32_t gps, gpr;                       // G[v][p(s)], G[v][p(r)] (pre-update)
-        tc::tmem_ld1(tm + quad_lane + TCS_COL_G + (uint32_t)ps, gps);
-        tc::tmem_ld1(tm + quad_lane + TCS_COL_G + (uint32_t)pr, gpr);
+        int dAu[4], dBfu[4];                     // dA of the next rows (locations), dBf of their facilities
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int u = min(nu0 + i, n - 1);
+            dAu[i] = (int)As[u * ld + r] - (int)As[u * ld + s];
+            dBfu[i] = (int)Bs[npu[i] * ld + pr] - (int)Bs[npu[i] * ld + ps];
+        }
+        const int ars = As[r * ld + s], brs = Bs[pr * ld + ps];
         const int ro = (v >> 3) * 256 + (v & 7) * 16;
         if (ENS) *reinterpret_cast<uint16_t*>(La + ro) = (uint16_t)(b8(dA) | (b8(-dBf) << 8));   // A row v
         else tc::tmem_st1(tm + quad_lane + TCS_COL_L, b8(dA) | (b8(-dBf) << 8));
         *reinterpret_cast<uint32_t*>(Rg + ro) = b8(-dBf);               // G rows: facility v
         *reinterpret_cast<uint32_t*>(Rg + 4096 + ro) = b8(dA) << 8;    // H rows: location v
-        const int ars = As[r * ld + s], brs = Bs[pr * ld + ps];
-        int nu0, nv0;                            // next window: cursor after (r, s)
-        next_pair(n, r, s, &nu0, &nv0);
         const int Wn = max(64, min(wmax, round_up32(8 * (j + 1))));
-        int Wln = win_total<4>(n, nu0, nv0);
-        if (Wn < Wln) Wln = Wn;
-        if (kacc + 1 + (uint64_t)Wln > k_end) Wln = (int)(k_end - kacc - 1);
-        const int npn = Wln < TCK_TH ? Wln : TCK_TH;
-        if (t == 0) {                            // the accept, for the helper warps
-            rec[0] = r; rec[1] = s;
-            rec[2] = (int)(uint32_t)kacc; rec[3] = (int)(uint32_t)(kacc >> 32);
-            rec[4] = npn;
+        if (t == 0) {                            // the accept, for the helper warps (buffer by accept parity:
+            int* rc = rec + 4 * (int)(accepted & 1);   // the helpers are at most one accept behind)
+            rc[0] = r; rc[1] = s;
+            rc[2] = (int)(uint32_t)kacc; rc[3] = (int)(uint32_t)(kacc >> 32);
         }
         tc::tmem_wait_ld();
+        if (hsh) {
+#pragma unroll
+            for (int i = 0; i < 3; ++i) h4[i] = hsh == 1 ? h4[i + 1] : (i < 2 ? h4[i + 2] : h4[3]);
+        }
         const int dnew = (v == r) ? (int)gps + ars * brs : (v == s) ? (int)gpr + ars * brs : dv - dA * dB;
-        TCT_ACC(3, pt1, dnew);
+        px = (v == r) ? ps : (v == s) ? pr : px;     // p(v), p^-1(v) after the swap
+        qv = (v == pr) ? s : (v == ps) ? r : qv;
+        const bool wrap = nu0 < r;               // cursor back at row 0: rows not staged
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            pu[i] = npu[i];
+            gv[i] = (uint32_t)((int)g4[i] - dA * dBfu[i]);                 // G''[v][p''(u_i)]
+            if (vin) xch[i * 128 + qv] = (int)h4[i] - dBf * dAu[i];       // H''[v][u_i] = G''_{u_i, p''^-1(v)}
+        }
+        if (vin) Dg[v] = dnew;
+        if (v == r) p[v] = (uint16_t)ps;
+        if (v == s) p[v] = (uint16_t)pr;
+        TCT_ACC(2, pt1, dnew);
         tc::fence_proxy_async();
         tc::tmem_wait_st();
         tc::fence_before_sync();
-        group_sync(1, TCS_NT);                   // operands staged; the helpers take the accept
-        TCT_ACC(4, pt1, p[0]);
-        if (t == 0) {
+        group_sync(1, TCS_NT);                   // operands staged, next rows exchanged: MMA issue
+        TCT_ACC(3, pt1, xch[v]);
+        mma_pending = true;
+        fresh = wrap;
+        cost += dw;
+        if (cost < best) {
+            best = cost;
+            if (vin) best_p[v] = (uint16_t)px;
+        }
+        u0 = nu0;
+        v0 = nv0;
+        W = Wn;
+        ++accepted;
+        k = kacc + 1;
+        k_last = k;
+        rejI = rej_bound(sch, k);
+        Tw = temp32(sch, k);
+    }
+    if (mma_pending) {                           // the last update complete before tensor memory is freed
+        tc::mbar_wait(mbar, ph);
+        ph ^= 1;
+        tc::fence_after_sync();
+    }
+    if (RING && t == 0) TR.drain();
+    if (t == 0) rec[4 * (int)(accepted & 1)] = -1;
+    group_sync(1, TCS_NT);                       // release the helpers
+  } else {
+    // ---------------- helper warps: the update MMA of each accept, digest ----------------
+    for (uint64_t na = 0;; ++na) {
+        group_sync(1, TCS_NT);
+        const int* rc = rec + 4 * (int)(na & 1);
+        const int r = rc[0];
+        if (r < 0) break;
+        if (t == 128) {
             tc::fence_after_sync();
             // [G | H] (256 columns) += [dA, -dBf] [[-dBf, 0]; [0, dA]]^T
             if (ENS)
@@ -334,53 +442,10 @@ __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, uns
             else
                 tc::mma_i8_ts(tm + TCS_COL_G, tm + TCS_COL_L, tc::smem_desc(tc::smem_u32(Rg), 128, 256), id_gh, true);
             tc::mma_commit(mbar);
+            const int s = rc[1];
+            const uint64_t kacc = (uint64_t)(uint32_t)rc[2] | ((uint64_t)(uint32_t)rc[3] << 32);
+            digest = digest_step(digest, kacc, r, s);
         }
-        if (vin) Dg[v] = dnew;
-        if (v == r) p[v] = (uint16_t)ps;
-        if (v == s) p[v] = (uint16_t)pr;
-        cost += dw;
-        const bool improved = cost < best;
-        if (improved) {
-            best = cost;
-            if (vin) best_p[v] = (uint16_t)((v == r) ? ps : (v == s) ? pr : px);
-        }
-        tc::mbar_wait(mbar, ph);                 // G, H updated before the next window reads them
-        ph ^= 1;
-        tc::fence_after_sync();
-        TCT_ACC(5, pt1, ph);
-        group_sync(2, 128);                      // D, p complete
-        TCT_ACC(6, pt1, Dg[0]);
-        TCT_ACC(7, pt0, Dg[1]);
-        px = (v == r) ? ps : (v == s) ? pr : px;
-        qv = (v == pr) ? s : (v == ps) ? r : qv;
-        pk = kacc + 1;
-        pn = npn;
-        u0 = nu0;
-        v0 = nv0;
-        W = Wn;
-        ++accepted;
-        k = kacc + 1;
-        k_last = k;
-        rejI = rej_bound(sch, k);
-    }
-    if (t == 0) rec[0] = -1;
-    group_sync(1, TCS_NT);                       // release the helpers
-  } else {
-    // ---------------- helper warps: thresholds of the window after each accept, digest ----------------
-    while (true) {
-        group_sync(1, TCS_NT);
-        const int r = rec[0];
-        if (r < 0) break;
-        const int s = rec[1], npn = rec[4];
-        const uint64_t kacc = (uint64_t)(uint32_t)rec[2] | ((uint64_t)(uint32_t)rec[3] << 32);
-        for (int o = v; o < npn; o += 128) {
-            float th, m;
-            theta_of(sch, seed, cv.chain, kacc + 1 + (uint64_t)o, &th, &m);
-            thm[o] = make_float2(th, m);
-        }
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(mbar_t);  // 4 helper warps: the thresholds are written
-        if (t == 128) digest = digest_step(digest, kacc, r, s);
     }
   }
 

@@ -45,6 +45,7 @@
 
 #include "kernels.cuh"
 #include "tc_common.cuh"
+#include "theta_ring.cuh"
 
 namespace qapsa {
 
@@ -70,7 +71,7 @@ __host__ __device__ __forceinline__ int cofs(int x, int k) {
 }
 
 struct TcLayout {
-    int a, b, rd, rg, rh, tmp, p, pinv, bestp, rowr, rows, xbuf, zbuf, slots, tile, thm, misc, bytes;
+    int a, b, rd, rg, rh, tmp, p, pinv, bestp, rowr, rows, xbuf, zbuf, slots, tile, thm, misc, tbar, bytes;
 };
 // ld: row stride of A and B (row_stride(n, true) <= 144)
 __host__ __device__ inline TcLayout tc_layout(int ld) {
@@ -81,7 +82,8 @@ __host__ __device__ inline TcLayout tc_layout(int ld) {
     o = (o + 1023) & ~1023;
     L.rd = o;    o += 128 * 32;                 // B operands, K-major canonical (SBO 256, LBO 128)
     L.rg = o;    o += 256 * 32;                 // G|H update: rows 0..127 G (facility), 128..255 H (location)
-    L.tmp = o;   o += 2 * 128 * 128;            // init only: A, C canonical (SBO 1024, LBO 128)
+    L.tmp = o;   o += 2 * 128 * 128;            // init: A, C canonical (SBO 1024, LBO 128); then the θ ring
+    static_assert(2 * 128 * 128 == TH_RING_BYTES, "the θ ring reuses the init operands");
     L.p = o;     o += 128 * 2;
     L.pinv = o;  o += 128 * 2;
     L.bestp = o; o += 128 * 2;
@@ -93,6 +95,7 @@ __host__ __device__ inline TcLayout tc_layout(int ld) {
     L.tile = o;  o += 4 * 4 * 32 * TCK_TILE * 4;   // helper warp x chunk patch tiles
     L.thm = o;   o += TCK_TH * 8;               // (θ, margin) by window offset
     L.misc = o;  o += 64;                       // mbarriers (2 x 8 B) | TMEM base (4 B)
+    L.tbar = o;  o += TH_SLOTS * 8;             // θ ring mbarriers
     L.bytes = o;
     return L;
 }
@@ -174,6 +177,7 @@ __device__ __noinline__ int tc_exact(int d, uint64_t kk, Sched sch, uint64_t see
 
 template <int NFIX, bool ENS = false>
 __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
+    constexpr bool RING = !ENS;                  // single chain: precomputed θ (theta_ring.cuh)
     extern __shared__ __align__(16) unsigned char smem[];
     const ChainView cv = chain_view<ENS>(a);     // this CTA's chain (ensemble launches)
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -264,6 +268,11 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
     tc::mbar_wait(mbar_g, 0);                    // G, H initialised
     uint32_t ph_d = 0;
     tc::fence_after_sync();
+    uint64_t k = cv.k0_dev ? *cv.k0_dev : a.k0, accepted = 0;
+    // single chain: θ of the window from the precomputed ring (reuses the init operands' space)
+    ThetaRing TR = theta_ring(reinterpret_cast<float*>(smem + L.tmp), reinterpret_cast<uint64_t*>(smem + L.tbar),
+                              a.theta, a.theta_kb, a.theta_cnt, k);
+    if (RING && t == 0 && k < a.k_end) TR.start(k);
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
@@ -273,7 +282,6 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
     const NearSink sink = cv.sink;
     int64_t cost = cv.st->cost, best = cv.st->best_cost;
     uint64_t digest = cv.st->digest;
-    uint64_t k = cv.k0_dev ? *cv.k0_dev : a.k0, accepted = 0;
     int u0, v0;
     tri_pair(n, (int)(k % (uint64_t)M), &u0, &v0);
     const int wmax = a.wmax;
@@ -282,6 +290,7 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
     // certain-reject bound: δ > 38.5 T32(k) >= 38.4 T_kk gives exp(-δ/T) < 2^-54 <= r (chain.cuh);
     // rounded up to an integer, so the exact test below also sees every δ <= 38.5 T32(k)
     int rejI = rej_bound(sch, k);
+    float Tw = temp32(sch, k);                   // T at the window's first iteration (ring margin)
     uint64_t pk = ~0ull;                         // window whose thresholds are in thm
     int pn = 0;                                  // ... for offsets [0, pn)
     int pend_r = -1, pend_s = -1;                // rows r, s whose TMEM cells (lane r|s, column < r|s)
@@ -301,6 +310,10 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
         {
             const uint64_t remaining = k_end - k;
             if ((uint64_t)Wl > remaining) Wl = (int)remaining;
+        }
+        if (RING) {
+            if (t == 0) TR.refill(k);
+            TR.ensure(k + (uint64_t)Wl);
         }
         int4* sl = slots + parity * TCK_NW;
         unsigned acc_mask = 0, near_mask = 0;
@@ -344,9 +357,6 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
                 am |= (unsigned)(ex && d <= 0) << i;
                 need |= (unsigned)(ex && d > 0 && d <= rejI) << i;   // above rejI: certain reject
             }
-#if defined(TC_EXP) && (TC_EXP & 2)
-            need = 0;
-#endif
             if (__any_sync(0xffffffffu, need != 0)) {
                 const int pnk = pk == k ? pn : 0;
 #pragma unroll
@@ -355,7 +365,8 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
                         const int o = rb[4 * g + i] + v;
                         const int d = (int)dd[i];
                         float th, m;
-                        if (o < pnk) { const float2 q = thm[o]; th = q.x; m = q.y; }
+                        if (RING) { th = TR.at(k + (uint64_t)o); m = 2e-4f * th + 2e-5f * Tw; }
+                        else if (o < pnk) { const float2 q = thm[o]; th = q.x; m = q.y; }
                         else theta_of(sch, seed, cv.chain, k + (uint64_t)o, &th, &m);
                         const float df = (float)d;
                         bool ac = df < th - m;
@@ -408,6 +419,7 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
             win_advance(n, u0, v0, Wl, &u0, &v0);
             W = min(2 * W, wmax);
             rejI = rej_bound(sch, k);
+            Tw = temp32(sch, k);
             continue;
         }
         const unsigned bw = __ballot_sync(0xffffffffu, tv == j);
@@ -504,7 +516,7 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
             int Wln = win_total(n, nu0, nv0);
             if (Wn < Wln) Wln = Wn;
             if (kacc + 1 + (uint64_t)Wln > k_end) Wln = (int)(k_end - kacc - 1);
-            for (int o = v; o < Wln && o < TCK_TH; o += 128) {
+            for (int o = v; !RING && o < Wln && o < TCK_TH; o += 128) {
                 float th, m;
                 theta_of(sch, seed, cv.chain, kacc + 1 + (uint64_t)o, &th, &m);
                 thm[o] = make_float2(th, m);
@@ -526,11 +538,7 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
             tc::fence_after_sync();
             const bool hr2 = (r >> 5) == (warp & 3), hs2 = (s >> 5) == (warp & 3);
             const int lim = hs2 ? s : (hr2 ? r : 0);   // columns [0, lim) hold row cells
-#if defined(TC_EXP) && (TC_EXP & 1)
-            if (false) {
-#else
             if (lim > 0) {                       // warp-uniform; chunks 32c .. 32c+31 for 32c < lim
-#endif
                 // Lane r (s) takes the whole chunk rows from rowR (rowS): its cells with column >= r
                 // (>= s) are upper-triangle cells, never read, so overwriting them is harmless;
                 // every other lane writes back what it read.
@@ -579,7 +587,9 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
         ++accepted;
         k = kacc + 1;
         rejI = rej_bound(sch, k);
+        Tw = temp32(sch, k);
     }
+    if (RING && t == 0) TR.drain();
 
     // ---------------- write the chain state back ----------------
 #ifdef QAPSA_PHASE_TIMERS

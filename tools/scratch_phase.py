@@ -34,8 +34,8 @@ ms, _ = s.last_kernel_time()
 L.qapsa_debug_phase_cycles(buf)
 na = max(1, buf[127])
 print(f"{ms*1e-3*1.965e9/na:.0f} clk per accept ({na} accepts in the first kernel)")
-names = ["window loads", "exchange barrier", "tests done", "stage done (from decision)", "staging barrier", "mbar",
-         "second barrier", "loop (top to end)"]
-for w in (0, 4):
+names = ["window values ready", "tests done (from loop top)", "stage done (from decision)",
+         "staging barrier passed (from decision)", "non-accepting windows (total)"]
+for w in (0,):
     b = buf[16 * w: 16 * w + 12]
     print(f"warp {w}: " + ", ".join(f"{nm} {b[i]/na:.0f}" for i, nm in enumerate(names) if b[i]))
