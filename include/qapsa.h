@@ -211,7 +211,8 @@ qap_status qap_start_perms(qap_ctx* ctx, uint64_t seed, uint32_t chain_begin, ui
 /* Tuning knobs.  Results never depend on them (window / CTA shape
  * invariance); they exist for the invariance tests and benchmarks. */
 typedef enum {
-    QAP_OPT_WINDOW_MAX = 1,      /* max candidates per window, 32..1024 (default 1024) */
+    QAP_OPT_WINDOW_MAX = 1,      /* max candidates per window, multiple of 32 in 32..8192 (default:
+                                    1024; the tensor-memory Δ engine scans whole rows, up to 7168) */
     QAP_OPT_THREADS = 2,         /* single-chain CTA threads: 0 = auto (default), 64..1024 */
     QAP_OPT_FORCE_GLOBAL_DELTA = 3, /* 1: keep Δ in global memory/L2 even if it fits on chip */
     QAP_OPT_ENSEMBLE_GROUP = 4,  /* threads per chain in qap_ensemble_run: 64, 128 or 256 */

@@ -219,6 +219,7 @@ struct ChainArgs {
     unsigned char* near_dec;
     int near_cap;
     int n, ld, M, wmax;
+    int wscan;               // Δ engine (k_sa_tc): window cap of its whole-row windows
     unsigned long long k0, k_end, seed;
     Sched sch;
     const unsigned long long* k0_dev;   // if set, k0 is read from device memory (chained launches)

@@ -48,7 +48,7 @@ struct qap_ctx {
     bool delta_valid = false;
     bool sticky = false;
     std::string err;
-    int wmax = 1024, threads = 0 /* auto */, force_global = 0, ens_group = 128;
+    int wmax = 0 /* auto */, threads = 0 /* auto */, force_global = 0, ens_group = 128;
     int smem_optin = 0, num_sms = 0;
     bool tc_ok = false;                 // instance fits the tensor-memory engine (tc_chain.cuh)
     int use_tc = 1;
@@ -542,7 +542,8 @@ qap_status qap_sa_run(qap_ctx* c, uint64_t k0, uint64_t iters, const qap_schedul
     a.near_count = c->dnear_count; a.near_k = c->dnear_k; a.near_dec = c->dnear_dec;
     a.near_cap = QAP_NEAR_LOG_CAP;
     a.near_chain = nullptr;
-    a.n = c->n; a.ld = c->ld; a.M = c->M; a.wmax = std::min(c->wmax, threads);
+    a.n = c->n; a.ld = c->ld; a.M = c->M; a.wmax = std::min(c->wmax ? c->wmax : 1024, threads);
+    a.wscan = c->wmax ? c->wmax : TCK_WSCAN;
     a.k0 = k0; a.k_end = k0 + iters; a.seed = seed; a.sch = sch;
 
     a.theta = nullptr;
@@ -566,7 +567,7 @@ qap_status qap_sa_run(qap_ctx* c, uint64_t k0, uint64_t iters, const qap_schedul
     a.switch_gap = 0;
     int launches = 0;
     if (tc) {
-        a.wmax = c->wmax;
+        a.wmax = c->wmax ? c->wmax : 1024;
         // compile-time problem size for the BASELINE configurations, generic otherwise
         auto kern = c->n == 100 ? k_sa_tc<100> : c->n == 50 ? k_sa_tc<50> : c->n == 12 ? k_sa_tc<12> : k_sa_tc<0>;
         CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -813,7 +814,8 @@ static qap_status ensemble_tc(qap_ctx* c, uint32_t chain_begin, uint32_t chain_c
     a.rowaddr = c->drowaddr; a.qdesc = c->dqdesc; a.nqt = c->nqt;
     a.near_count = c->ens_near_count; a.near_k = c->ens_near_k; a.near_dec = c->ens_near_dec;
     a.near_chain = c->ens_near_chain; a.near_cap = QAP_ENS_NEAR_LOG_CAP;
-    a.n = n; a.ld = c->ld; a.M = c->M; a.wmax = c->wmax;
+    a.n = n; a.ld = c->ld; a.M = c->M; a.wmax = c->wmax ? c->wmax : 1024;
+    a.wscan = c->wmax ? c->wmax : TCK_WSCAN;
     a.k0 = 0; a.k_end = iters; a.seed = seed; a.sch = sch;
     a.k0_dev = nullptr; a.proposal = 0;
     a.ens = 1; a.dstride = dstride; a.chain = chain_begin;
@@ -929,7 +931,7 @@ qap_status qap_ensemble_run(qap_ctx* c, uint32_t chain_begin, uint32_t chain_cou
     a.next_chain = c->ens_counter; a.count = (int)chain_count; a.n = n; a.ld = c->ld; a.M = c->M;
     a.rowaddr = c->drowaddr; a.qdesc = c->dqdesc; a.nqt = c->nqt;
     a.proposal = c->proposal;
-    a.wmax = std::min(c->wmax, nt); a.chain_begin = chain_begin; a.iters = iters; a.seed = seed; a.sch = sch;
+    a.wmax = std::min(c->wmax ? c->wmax : 1024, nt); a.chain_begin = chain_begin; a.iters = iters; a.seed = seed; a.sch = sch;
     a.near_count = c->ens_near_count; a.near_k = c->ens_near_k; a.near_dec = c->ens_near_dec;
     a.near_chain = c->ens_near_chain; a.near_cap = QAP_ENS_NEAR_LOG_CAP;
     CU(cudaEventRecord(c->ev0, c->stream));
@@ -1016,7 +1018,7 @@ qap_status qap_set_option(qap_ctx* c, int32_t key, int64_t value) {
     CHECK_CTX(c);
     switch (key) {
         case QAP_OPT_WINDOW_MAX:
-            if (value < 32 || value > 1024 || (value & 31)) return fail(c, QAP_E_INVALID_ARG, "window must be a multiple of 32 in [32,1024]");
+            if (value < 32 || value > 8192 || (value & 31)) return fail(c, QAP_E_INVALID_ARG, "window must be a multiple of 32 in [32,8192]");
             c->wmax = (int)value;
             return QAP_OK;
         case QAP_OPT_THREADS:

@@ -29,7 +29,8 @@
 
 namespace qapsa {
 
-constexpr int TCS_NT = 256;
+constexpr int TCS_NT = 288;            // 8 row warps (two window rows each) + 1 helper warp
+constexpr int TCS_RW = 8;              // row warps
 constexpr uint32_t TCS_COL_G = 0;        // G: TMEM columns [0, 128)
 constexpr uint32_t TCS_COL_H = 128;      // H: TMEM columns [128, 256)
 constexpr uint32_t TCS_COL_L = 256;      // single chain: A operand of the update [dA, -dBf] (K = 32)
@@ -54,7 +55,7 @@ __host__ __device__ inline ScLayout sc_layout(int ld) {
     L.bestp = o; o += 128 * 2;
     L.dg = o;    o += 128 * 4;                  // D_x
     L.xch = o;   o += 4 * 128 * 4;              // G[u_i][p(v)] by window row i and location v
-    L.slots = o; o += 2 * 4 * 16;
+    L.slots = o; o += 2 * TCS_RW * 16;
     L.rec = o;   o += 32;                       // the accept for the helpers, double-buffered
     L.misc = o;  o += 64;                       // mbarrier | TMEM base
     L.tbar = o;  o += TH_SLOTS * 8;             // θ ring mbarriers
@@ -63,7 +64,7 @@ __host__ __device__ inline ScLayout sc_layout(int ld) {
 }
 
 template <int NFIX, bool ENS = false>
-__global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, unsigned long long* k_out) {
+__global__ void __launch_bounds__(TCS_NT, ENS ? 2 : 1) k_sa_scratch(const ChainArgs a, unsigned long long* k_out) {
     constexpr bool RING = !ENS;                  // single chain: precomputed θ (theta_ring.cuh)
     extern __shared__ __align__(16) unsigned char smem[];
     const ChainView cv = chain_view<ENS>(a);     // this CTA's chain (ensemble launches)
@@ -84,7 +85,9 @@ __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, uns
     int* rec = reinterpret_cast<int*>(smem + L.rec);
     uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + L.misc);          // G|H update done
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.misc + 8);
-    const bool lanew = warp < 4;
+    const bool lanew = warp < 4;                 // lane warps: thread v owns TMEM lane v (one per v)
+    const bool roww = warp < TCS_RW;             // row warps: window rows 2h, 2h + 1 (h = warp / 4)
+    const int h2 = 2 * (warp >> 2);
     const uint32_t quad_lane = (uint32_t)(32 * (warp & 3)) << 16;
     const int v = t & 127;
     const bool vin = v < n;
@@ -145,7 +148,7 @@ __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, uns
     uint32_t ph = 1;
     tc::fence_after_sync();
     // single chain: θ of the window from the precomputed ring (reuses the init operands' space)
-    ThetaRing TR = theta_ring(reinterpret_cast<float*>(smem + L.tmp), reinterpret_cast<uint64_t*>(smem + L.tbar),
+    ThetaRing<TH_SLOTS> TR = theta_ring<TH_SLOTS>(reinterpret_cast<float*>(smem + L.tmp), reinterpret_cast<uint64_t*>(smem + L.tbar),
                               a.theta, a.theta_kb, a.theta_cnt, a.k0);
     if (RING && t == 0 && a.k0 < a.k_end) TR.start(a.k0);
     __syncthreads();
@@ -161,24 +164,25 @@ __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, uns
     const int wmax = a.wmax;
     int W = wmax;
     int parity = 0;
-    int rejI = rej_bound(sch, k);
     float Tw = temp32(sch, k);                   // T at the window's first iteration (ring margin)
+    int rejI = rej_of(Tw);
     const uint32_t id_gh = tc::idesc_i8(128, 256, true);
 #ifdef QAPSA_PHASE_TIMERS
     long long tacc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 #endif
 
-  if (lanew) {
+  if (roww) {
     const uint64_t gap = a.switch_gap ? a.switch_gap : TCS_SWITCH_GAP;
-    // The window's rows u_i = u0 + i: pu[i] = p(u_i), gv[i] = G[v][p(u_i)] (registers) and
-    // xch[i][v] = G_{u_i, v} (shared memory).  After an accept they are produced by the stage from
-    // the PRE-update tensor memory plus the exact rank-1 change of the accept, so the next window
-    // is tested while the tensor cores apply that change (the MMA is waited for only before the
-    // next read or write of tensor memory); after a window without accept they are read afresh.
+    // The window's rows u_i = u0 + i, i < 4; this warp's are i = h2 + e, e < 2: pu[e] = p(u_i),
+    // gv[e] = G[v][p(u_i)] (registers) and xch[i][v] = G_{u_i, v} (shared memory).  After an
+    // accept they are produced by the stage from the PRE-update tensor memory plus the exact rank-1
+    // change of the accept, so the next window is tested while the tensor cores apply that change
+    // (the MMA is waited for only before the next read or write of tensor memory); after a window
+    // without accept they are read afresh.
     bool fresh = true;
     bool mma_pending = false;
-    int pu[4];
-    uint32_t gv[4];
+    int pu[2];
+    uint32_t gv[2];
     while (k < k_end && k - k_last < gap) {
         // ---------------- window: rows u0 .. u0+R-1 (R <= 4) ----------------
         TCT_MARK(pt0, u0 + v0);
@@ -193,15 +197,12 @@ __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, uns
             if (t == 0) TR.refill(k);
             TR.ensure(k + (uint64_t)Wl);
         }
-        int rb[4], rf[4];
-        {
-            int f = 0;
+        int rb[2], rf[2];                        // offset base and first column of rows h2, h2 + 1
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                rf[i] = i == 0 ? v0 : u0 + i + 1;
-                rb[i] = f - rf[i];
-                f += i == 0 ? L0 : m1 - i;
-            }
+        for (int e = 0; e < 2; ++e) {
+            const int i = h2 + e;
+            rf[e] = i == 0 ? v0 : u0 + i + 1;
+            rb[e] = (i == 0 ? 0 : win_f(i, L0, m1)) - rf[e];
         }
         if (fresh) {
             if (mma_pending) {                   // G, H complete before they are read
@@ -210,109 +211,99 @@ __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, uns
                 tc::fence_after_sync();
                 mma_pending = false;
             }
-            uint32_t hf[4];                      // H[f][u_i] (facility lane f = v)
+            uint32_t hf[2];                      // H[f][u_i] (facility lane f = v)
 #pragma unroll
-            for (int i = 0; i < 4; ++i) pu[i] = p[min(u0 + i, n - 1)];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) tc::tmem_ld1(tm + quad_lane + TCS_COL_G + (uint32_t)pu[i], gv[i]);
-            // H columns u0 .. u0+3 must stay inside [TCS_COL_H, TCS_COL_H + 128) (an ensemble CTA owns
-            // only 256 columns): read from hb = min(u0, 124) and shift (rows past n-1 are never used)
-            const int hb = min(u0, 124), hsh = u0 - hb;
-            tc::tmem_ld4(tm + quad_lane + TCS_COL_H + (uint32_t)hb, hf);
-            tc::tmem_wait_ld();
-            if (hsh) {                           // warp-uniform, only in the last rows of the triangle
-#pragma unroll
-                for (int i = 0; i < 3; ++i) hf[i] = hsh == 1 ? hf[i + 1] : (i < 2 ? hf[i + 2] : hf[3]);
+            for (int e = 0; e < 2; ++e) {
+                const int u = min(u0 + h2 + e, n - 1);   // rows past n-1 are never used
+                pu[e] = p[u];
+                tc::tmem_ld1(tm + quad_lane + TCS_COL_G + (uint32_t)pu[e], gv[e]);
+                tc::tmem_ld1(tm + quad_lane + TCS_COL_H + (uint32_t)u, hf[e]);
             }
+            tc::tmem_wait_ld();
             if (vin) {
 #pragma unroll
-                for (int i = 0; i < 4; ++i) xch[i * 128 + qv] = (int)hf[i];   // G[u_i][v] to location p^-1(v)
+                for (int e = 0; e < 2; ++e) xch[(h2 + e) * 128 + qv] = (int)hf[e];   // G[u_i][v] to location p^-1(v)
             }
-            group_sync(3, 128);                  // exchange
+            group_sync(3, 32 * TCS_RW);          // exchange
         }
         TCT_ACC(0, pt0, xch[v]);
-        int4* sl = slots + parity * 4;
+        int4* sl = slots + parity * TCS_RW;
         unsigned acc_mask = 0, near_mask = 0;
         const int dv = Dg[v];
         unsigned need = 0;
-        int dd[4];
+        int dd[2];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int e = 0; e < 2; ++e) {
+            const int i = h2 + e;
             const int u = min(u0 + i, n - 1);
             const int guv = xch[i * 128 + v];                   // G_uv = (A B'^T)[u][v]
-            const int auv = As[u * ld + v], buv = Bs[pu[i] * ld + px];
-            dd[i] = 2 * (guv + (int)gv[i] - Dg[u] - dv + 2 * auv * buv);   // δ(u, v) (R10d)
-            const int o = rb[i] + v;
-            const bool ex = i < R && v >= rf[i] && vin && o < Wl;
-            acc_mask |= (unsigned)(ex && dd[i] <= 0) << i;      // δ <= 0 (R5)
-            need |= (unsigned)(ex && dd[i] > 0 && dd[i] <= rejI) << i;
+            const int auv = As[u * ld + v], buv = Bs[pu[e] * ld + px];
+            dd[e] = 2 * (guv + (int)gv[e] - Dg[u] - dv + 2 * auv * buv);   // δ(u, v) (R10d)
+            const int o = rb[e] + v;
+            const bool ex = i < R && v >= rf[e] && vin && o < Wl;
+            acc_mask |= (unsigned)(ex && dd[e] <= 0) << e;      // δ <= 0 (R5)
+            need |= (unsigned)(ex && dd[e] > 0 && dd[e] <= rejI) << e;
         }
         if (RING) {                              // branch-free θ test; the exact path only inside the margin
             unsigned band = 0;
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int o = rb[i] + v;
+            for (int e = 0; e < 2; ++e) {
+                const int o = rb[e] + v;
                 const float th = TR.at(k + (uint64_t)max(o, 0));
                 const float m = 2e-4f * th + 2e-5f * Tw;
-                const float df = (float)dd[i];
-                const bool nd = (need >> i) & 1u;
-                acc_mask |= (unsigned)(nd && df < th - m) << i;
-                band |= (unsigned)(nd && !(df < th - m) && !(df > th + m)) << i;
+                const float df = (float)dd[e];
+                const bool nd = (need >> e) & 1u;
+                acc_mask |= (unsigned)(nd && df < th - m) << e;
+                band |= (unsigned)(nd && !(df < th - m) && !(df > th + m)) << e;
             }
             if (__any_sync(0xffffffffu, band != 0)) {
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    if ((band >> i) & 1u) {      // inside the margin: exact double test (R16)
-                        const int x = tc_exact(dd[i], k + (uint64_t)(rb[i] + v), sch, seed, cv.chain);
-                        acc_mask |= (unsigned)(x & 1) << i;
-                        near_mask |= (unsigned)((x >> 1) & 1) << i;
+                for (int e = 0; e < 2; ++e) {
+                    if ((band >> e) & 1u) {      // inside the margin: exact double test (R16)
+                        const int x = tc_exact(dd[e], k + (uint64_t)(rb[e] + v), sch, seed, cv.chain);
+                        acc_mask |= (unsigned)(x & 1) << e;
+                        near_mask |= (unsigned)((x >> 1) & 1) << e;
                     }
                 }
             }
         } else if (__any_sync(0xffffffffu, need != 0)) {
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                if ((need >> i) & 1u) {
-                    const int o = rb[i] + v;
+            for (int e = 0; e < 2; ++e) {
+                if ((need >> e) & 1u) {
+                    const int o = rb[e] + v;
                     float th, m;
                     theta_of(sch, seed, cv.chain, k + (uint64_t)o, &th, &m);
-                    const float df = (float)dd[i];
+                    const float df = (float)dd[e];
                     bool ac = df < th - m;
                     if (!ac && !(df > th + m)) {  // inside the margin: exact double test (R16)
-                        const int x = tc_exact(dd[i], k + (uint64_t)o, sch, seed, cv.chain);
+                        const int x = tc_exact(dd[e], k + (uint64_t)o, sch, seed, cv.chain);
                         ac = x & 1;
-                        near_mask |= (unsigned)((x >> 1) & 1) << i;
+                        near_mask |= (unsigned)((x >> 1) & 1) << e;
                     }
-                    acc_mask |= (unsigned)ac << i;
+                    acc_mask |= (unsigned)ac << e;
                 }
             }
         }
-        int best_o = INT_MAX, best_d = 0, best_rs = 0;
-#pragma unroll
-        for (int i = 3; i >= 0; --i) {
-            const bool ac = (acc_mask >> i) & 1u;
-            best_o = ac ? rb[i] + v : best_o;
-            best_d = ac ? dd[i] : best_d;
-            best_rs = ac ? ((u0 + i) | (v << 8) | (pu[i] << 16) | (px << 24)) : best_rs;
-        }
-        {
+        {   // this thread's first accepted candidate (row h2 before row h2 + 1)
+            const int e = (acc_mask & 1u) ? 0 : 1;
+            const int best_o = acc_mask ? rb[e] + v : INT_MAX;
             const int wmin = __reduce_min_sync(0xffffffffu, best_o);
-            if (best_o == wmin && (wmin != INT_MAX || lane == 0)) sl[warp] = make_int4(best_o, best_d, best_rs, 0);
+            if (best_o == wmin && (wmin != INT_MAX || lane == 0))
+                sl[warp] = make_int4(best_o, dd[e], (u0 + h2 + e) | (v << 8) | (pu[e] << 16) | (px << 24), 0);
         }
         TCT_ACC(1, pt0, acc_mask);
-        group_sync(4, 128);                      // window decision
-        const int tv = lane < 4 ? sl[lane].x : INT_MAX;
+        group_sync(4, 32 * TCS_RW);              // window decision
+        const int tv = lane < TCS_RW ? sl[lane].x : INT_MAX;
         const int j = __reduce_min_sync(0xffffffffu, tv);
         TCT_MARK(pt1, j);
+        TCT_ACC(10, pt0, j);
         parity ^= 1;
-        const int consumed = (j == INT_MAX) ? Wl : j + 1;
         if (near_mask) {                         // R16: log near ties of consumed iterations
+            const int consumed = (j == INT_MAX) ? Wl : j + 1;
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int o = rb[i] + v;
-                if (((near_mask >> i) & 1u) && o < consumed) {
-                    near_record(sink, k + (uint64_t)o, (acc_mask >> i) & 1u);
-                }
+            for (int e = 0; e < 2; ++e) {
+                const int o = rb[e] + v;
+                if (((near_mask >> e) & 1u) && o < consumed) near_record(sink, k + (uint64_t)o, (acc_mask >> e) & 1u);
             }
         }
         if (j == INT_MAX) {
@@ -320,8 +311,8 @@ __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, uns
             k += (uint64_t)Wl;
             win_advance<4>(n, u0, v0, Wl, &u0, &v0);
             W = min(2 * W, wmax);
-            rejI = rej_bound(sch, k);
             Tw = temp32(sch, k);
+            rejI = rej_of(Tw);
             fresh = true;
             continue;
         }
@@ -331,74 +322,84 @@ __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, uns
         const int r = win.z & 0xFF, s = (win.z >> 8) & 0xFF;
         const int pr = (win.z >> 16) & 0xFF, ps = (int)((unsigned)win.z >> 24);
         const uint64_t kacc = k + (uint64_t)j;
+        TCT_ACC(5, pt1, r + ps);
         // ---------------- stage: the G|H update operands, D'', the next window's rows ----------------
         int nu0, nv0;                            // next window: cursor after (r, s)
         next_pair(n, r, s, &nu0, &nv0);
-        int npu[4];                              // facilities of the next window's rows after the swap
+        int npu[2], nu[2];                       // this warp's next rows and their facilities after the swap
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int u = min(nu0 + i, n - 1);
-            npu[i] = u == r ? ps : u == s ? pr : (int)p[u];
+        for (int e = 0; e < 2; ++e) {
+            nu[e] = min(nu0 + h2 + e, n - 1);
+            npu[e] = nu[e] == r ? ps : nu[e] == s ? pr : (int)p[nu[e]];
         }
+        TCT_ACC(6, pt1, npu[0] + npu[1]);
         if (mma_pending) {                       // the previous update complete: tensor memory is current
             tc::mbar_wait(mbar, ph);
             ph ^= 1;
             tc::fence_after_sync();
         }
-        uint32_t gps, gpr, g4[4], h4[4];         // PRE-update tensor memory
-        tc::tmem_ld1(tm + quad_lane + TCS_COL_G + (uint32_t)ps, gps);   // G[v][p(s)]
-        tc::tmem_ld1(tm + quad_lane + TCS_COL_G + (uint32_t)pr, gpr);   // G[v][p(r)]
+        TCT_ACC(7, pt1, ph);
+        uint32_t gps = 0, gpr = 0, g4[2], h4[2];   // PRE-update tensor memory
+        if (h2 == 0) {
+            tc::tmem_ld1(tm + quad_lane + TCS_COL_G + (uint32_t)ps, gps);   // G[v][p(s)]
+            tc::tmem_ld1(tm + quad_lane + TCS_COL_G + (uint32_t)pr, gpr);   // G[v][p(r)]
+        }
 #pragma unroll
-        for (int i = 0; i < 4; ++i) tc::tmem_ld1(tm + quad_lane + TCS_COL_G + (uint32_t)npu[i], g4[i]);
-        const int hb = min(nu0, 124), hsh = nu0 - hb;
-        tc::tmem_ld4(tm + quad_lane + TCS_COL_H + (uint32_t)hb, h4);
-        int arv = 0, asv = 0, brv = 0, bsv = 0, bfr = 0, bfs = 0;
+        for (int e = 0; e < 2; ++e) {
+            tc::tmem_ld1(tm + quad_lane + TCS_COL_G + (uint32_t)npu[e], g4[e]);
+            tc::tmem_ld1(tm + quad_lane + TCS_COL_H + (uint32_t)nu[e], h4[e]);
+        }
+        int arv = 0, asv = 0, bfr = 0, bfs = 0;
         if (vin) {
             arv = As[r * ld + v]; asv = As[s * ld + v];
-            brv = Bs[pr * ld + px]; bsv = Bs[ps * ld + px];
             bfr = Bs[pr * ld + v]; bfs = Bs[ps * ld + v];
         }
-        const int dA = arv - asv, dB = brv - bsv, dBf = bfr - bfs;
-        int dAu[4], dBfu[4];                     // dA of the next rows (locations), dBf of their facilities
+        const int dA = arv - asv, dBf = bfr - bfs;
+        int dAu[2], dBfu[2];                     // dA of the next rows (locations), dBf of their facilities
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int u = min(nu0 + i, n - 1);
-            dAu[i] = (int)As[u * ld + r] - (int)As[u * ld + s];
-            dBfu[i] = (int)Bs[npu[i] * ld + pr] - (int)Bs[npu[i] * ld + ps];
+        for (int e = 0; e < 2; ++e) {
+            dAu[e] = (int)As[nu[e] * ld + r] - (int)As[nu[e] * ld + s];
+            dBfu[e] = (int)Bs[npu[e] * ld + pr] - (int)Bs[npu[e] * ld + ps];
         }
-        const int ars = As[r * ld + s], brs = Bs[pr * ld + ps];
-        const int ro = (v >> 3) * 256 + (v & 7) * 16;
-        if (ENS) *reinterpret_cast<uint16_t*>(La + ro) = (uint16_t)(b8(dA) | (b8(-dBf) << 8));   // A row v
-        else tc::tmem_st1(tm + quad_lane + TCS_COL_L, b8(dA) | (b8(-dBf) << 8));
-        *reinterpret_cast<uint32_t*>(Rg + ro) = b8(-dBf);               // G rows: facility v
-        *reinterpret_cast<uint32_t*>(Rg + 4096 + ro) = b8(dA) << 8;    // H rows: location v
+        if (h2 == 0) {                           // the update's operands (one thread per v)
+            const int ro = (v >> 3) * 256 + (v & 7) * 16;
+            if (ENS) *reinterpret_cast<uint16_t*>(La + ro) = (uint16_t)(b8(dA) | (b8(-dBf) << 8));   // A row v
+            else tc::tmem_st1(tm + quad_lane + TCS_COL_L, b8(dA) | (b8(-dBf) << 8));
+            *reinterpret_cast<uint32_t*>(Rg + ro) = b8(-dBf);               // G rows: facility v
+            *reinterpret_cast<uint32_t*>(Rg + 4096 + ro) = b8(dA) << 8;    // H rows: location v
+        }
         const int Wn = max(64, min(wmax, round_up32(8 * (j + 1))));
-        if (t == 0) {                            // the accept, for the helper warps (buffer by accept parity:
-            int* rc = rec + 4 * (int)(accepted & 1);   // the helpers are at most one accept behind)
+        if (t == 0) {                            // the accept, for the helper warp (buffer by accept parity:
+            int* rc = rec + 4 * (int)(accepted & 1);   // the helper is at most one accept behind)
             rc[0] = r; rc[1] = s;
             rc[2] = (int)(uint32_t)kacc; rc[3] = (int)(uint32_t)(kacc >> 32);
         }
-        tc::tmem_wait_ld();
-        if (hsh) {
-#pragma unroll
-            for (int i = 0; i < 3; ++i) h4[i] = hsh == 1 ? h4[i + 1] : (i < 2 ? h4[i + 2] : h4[3]);
+        TCT_ACC(9, pt1, dAu[1] + dBfu[1] + arv + bfs);
+        if (h2 == 0) {                           // D'' (one thread per v)
+            int dB = 0;
+            if (vin) dB = (int)Bs[pr * ld + px] - (int)Bs[ps * ld + px];
+            const int ars = As[r * ld + s], brs = Bs[pr * ld + ps];
+            tc::tmem_wait_ld();
+            const int dnew = (v == r) ? (int)gps + ars * brs : (v == s) ? (int)gpr + ars * brs : dv - dA * dB;
+            if (vin) Dg[v] = dnew;
+            if (v == r) p[v] = (uint16_t)ps;
+            if (v == s) p[v] = (uint16_t)pr;
+        } else {
+            tc::tmem_wait_ld();
         }
-        const int dnew = (v == r) ? (int)gps + ars * brs : (v == s) ? (int)gpr + ars * brs : dv - dA * dB;
+        TCT_ACC(8, pt1, (int)(h4[1] + g4[1]));
         px = (v == r) ? ps : (v == s) ? pr : px;     // p(v), p^-1(v) after the swap
         qv = (v == pr) ? s : (v == ps) ? r : qv;
         const bool wrap = nu0 < r;               // cursor back at row 0: rows not staged
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            pu[i] = npu[i];
-            gv[i] = (uint32_t)((int)g4[i] - dA * dBfu[i]);                 // G''[v][p''(u_i)]
-            if (vin) xch[i * 128 + qv] = (int)h4[i] - dBf * dAu[i];       // H''[v][u_i] = G''_{u_i, p''^-1(v)}
+        for (int e = 0; e < 2; ++e) {
+            pu[e] = npu[e];
+            gv[e] = (uint32_t)((int)g4[e] - dA * dBfu[e]);                 // G''[v][p''(u_i)]
+            if (vin) xch[(h2 + e) * 128 + qv] = (int)h4[e] - dBf * dAu[e];  // H''[v][u_i] = G''_{u_i, p''^-1(v)}
         }
-        if (vin) Dg[v] = dnew;
-        if (v == r) p[v] = (uint16_t)ps;
-        if (v == s) p[v] = (uint16_t)pr;
-        TCT_ACC(2, pt1, dnew);
+        TCT_ACC(2, pt1, gv[1]);
+        if (h2 == 0 && !ENS) tc::tmem_wait_st();
         tc::fence_proxy_async();
-        tc::tmem_wait_st();
         tc::fence_before_sync();
         group_sync(1, TCS_NT);                   // operands staged, next rows exchanged: MMA issue
         TCT_ACC(3, pt1, xch[v]);
@@ -407,7 +408,7 @@ __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, uns
         cost += dw;
         if (cost < best) {
             best = cost;
-            if (vin) best_p[v] = (uint16_t)px;
+            if (h2 == 0 && vin) best_p[v] = (uint16_t)px;
         }
         u0 = nu0;
         v0 = nv0;
@@ -415,8 +416,8 @@ __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, uns
         ++accepted;
         k = kacc + 1;
         k_last = k;
-        rejI = rej_bound(sch, k);
         Tw = temp32(sch, k);
+        rejI = rej_of(Tw);
     }
     if (mma_pending) {                           // the last update complete before tensor memory is freed
         tc::mbar_wait(mbar, ph);
@@ -425,15 +426,15 @@ __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, uns
     }
     if (RING && t == 0) TR.drain();
     if (t == 0) rec[4 * (int)(accepted & 1)] = -1;
-    group_sync(1, TCS_NT);                       // release the helpers
+    group_sync(1, TCS_NT);                       // release the helper
   } else {
-    // ---------------- helper warps: the update MMA of each accept, digest ----------------
+    // ---------------- helper warp: the update MMA of each accept, digest ----------------
     for (uint64_t na = 0;; ++na) {
         group_sync(1, TCS_NT);
         const int* rc = rec + 4 * (int)(na & 1);
         const int r = rc[0];
         if (r < 0) break;
-        if (t == 128) {
+        if (lane == 0) {
             tc::fence_after_sync();
             // [G | H] (256 columns) += [dA, -dBf] [[-dBf, 0]; [0, dA]]^T
             if (ENS)
@@ -468,7 +469,7 @@ __global__ void __launch_bounds__(TCS_NT, 1) k_sa_scratch(const ChainArgs a, uns
         ko[0] = k;                               // iteration reached (the Δ engine starts here)
         ko[1] = accepted;                        // swaps accepted in this phase
     }
-    if (t == 128) cv.st->digest = digest;
+    if (t == 32 * TCS_RW) cv.st->digest = digest;    // helper lane 0 holds the digest
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();

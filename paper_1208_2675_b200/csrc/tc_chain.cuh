@@ -27,8 +27,7 @@
 //   MMA     one thread issues the three updates (M = N = 128, K = 32 each).
 //   epilog  thread v: δ''(r,v), δ''(s,v) (R10b), D''_v = D_v - dA_v dB_v; the cells
 //           (lane v, column r|s) are column writes; the cells (lane r|s, column v < r|s) lie in
-//           one TMEM lane and are patched by a read-modify-write of the 32-lane block through a
-//           per-warp smem tile.  p, p^-1, best, digest.
+//           one TMEM lane and are patched by a read-modify-write of the 32-lane block (registers).  p, p^-1, best, digest.
 // The 4 helper warps compute the thresholds θ of the next window meanwhile.
 //
 // Window of candidates ("the swap which would have been found first"): the
@@ -51,13 +50,13 @@ namespace qapsa {
 
 constexpr int TCK_NT = 256;              // 8 warps: 4 lane warps (thread v <-> TMEM lane v), 4 helpers
 constexpr int TCK_NW = 8;                // warps: window slots
-constexpr int TCK_WR = 16;               // window rows (8 per half of the CTA, two tcgen05.ld of 4 columns)
+constexpr int TCK_WSCAN = 7168;          // window cap of the Δ engine (whole rows, cold phase): 7 θ blocks,
+                                         // TH_SLOTS_TC - 8 blocks of prefetch
 constexpr int TCK_TH = 256;              // thresholds prepared ahead per window (offsets < TCK_TH)
 constexpr uint32_t TCK_COL_G = 128;      // G: TMEM columns [128, 256)
 constexpr uint32_t TCK_COL_H = 256;      // H = G^T: TMEM columns [256, 384)
 constexpr uint32_t TCK_COL_L = 384;      // L operands (A from TMEM): Δ [384,392), G|H [392,400)
 constexpr uint32_t TCK_COLS = 512;       // TMEM columns allocated
-constexpr int TCK_TILE = 36;             // patch tile row stride in words (conflict-free 16 B rows)
 
 __host__ __device__ constexpr bool tc_eligible(int n, int maxA, int maxB) {
     return n >= 4 && n <= 128 && maxA <= 127 && maxB <= 127;
@@ -71,7 +70,7 @@ __host__ __device__ __forceinline__ int cofs(int x, int k) {
 }
 
 struct TcLayout {
-    int a, b, rd, rg, rh, tmp, p, pinv, bestp, rowr, rows, xbuf, zbuf, slots, tile, thm, misc, tbar, bytes;
+    int a, b, rd, rg, rh, tmp, p, pinv, bestp, rowr, rows, xbuf, zbuf, slots, thm, misc, tbar, bytes;
 };
 // ld: row stride of A and B (row_stride(n, true) <= 144)
 __host__ __device__ inline TcLayout tc_layout(int ld) {
@@ -82,8 +81,8 @@ __host__ __device__ inline TcLayout tc_layout(int ld) {
     o = (o + 1023) & ~1023;
     L.rd = o;    o += 128 * 32;                 // B operands, K-major canonical (SBO 256, LBO 128)
     L.rg = o;    o += 256 * 32;                 // G|H update: rows 0..127 G (facility), 128..255 H (location)
-    L.tmp = o;   o += 2 * 128 * 128;            // init: A, C canonical (SBO 1024, LBO 128); then the θ ring
-    static_assert(2 * 128 * 128 == TH_RING_BYTES, "the θ ring reuses the init operands");
+    L.tmp = o;   o += TH_SLOTS_TC * TH_BLK * 4;  // init: A, C canonical (SBO 1024, LBO 128); then the θ ring
+    static_assert(2 * 128 * 128 <= TH_SLOTS_TC * TH_BLK * 4, "the θ ring reuses the init operands");
     L.p = o;     o += 128 * 2;
     L.pinv = o;  o += 128 * 2;
     L.bestp = o; o += 128 * 2;
@@ -92,10 +91,9 @@ __host__ __device__ inline TcLayout tc_layout(int ld) {
     L.xbuf = o;  o += 128 * 8;
     L.zbuf = o;  o += 16;
     L.slots = o; o += 2 * TCK_NW * 16;
-    L.tile = o;  o += 4 * 4 * 32 * TCK_TILE * 4;   // helper warp x chunk patch tiles
     L.thm = o;   o += TCK_TH * 8;               // (θ, margin) by window offset
     L.misc = o;  o += 64;                       // mbarriers (2 x 8 B) | TMEM base (4 B)
-    L.tbar = o;  o += TH_SLOTS * 8;             // θ ring mbarriers
+    L.tbar = o;  o += TH_SLOTS_TC * 8;          // θ ring mbarriers
     L.bytes = o;
     return L;
 }
@@ -121,14 +119,30 @@ __device__ __forceinline__ uint32_t pack8(int a, int b, int c, int d) {
 __device__ __forceinline__ int win_f(int i, int L0, int m1) {   // f_i for i >= 1
     return L0 + (i - 1) * m1 - (((i - 1) * i) >> 1);
 }
-template <int RMAX = TCK_WR>
+template <int RMAX>
 __device__ __forceinline__ int win_rows(int n, int u0) { return min(RMAX, n - 1 - u0); }
-template <int RMAX = TCK_WR>
+template <int RMAX>
 __device__ __forceinline__ int win_total(int n, int u0, int v0) {
     return win_f(win_rows<RMAX>(n, u0), n - v0, n - 1 - u0);
 }
+// Δ engine: the number R >= 1 of whole rows from the cursor (the first from v0) whose candidates
+// f_R fit in W (at least the first row); R <= n - 1 - u0 (the window never wraps).  The quadratic
+// f_{x+1} = L0 + x m1 - x (x + 1) / 2 <= W is solved in float and corrected exactly.
+__device__ __forceinline__ int win_rows_whole(int n, int u0, int L0, int m1, int W) {
+    const int Rmax = n - 1 - u0;
+    if (W <= L0 || Rmax <= 1) return 1;
+    const float b = 2.0f * (float)m1 - 1.0f;
+    const float disc = b * b - 8.0f * (float)(W - L0);
+    int R = disc < 0.0f ? Rmax : min(Rmax, (int)(0.5f * (b - sqrtf(disc))) + 1);
+    R = max(R, 1);
+#pragma unroll 1
+    while (R < Rmax && win_f(R + 1, L0, m1) <= W) ++R;
+#pragma unroll 1
+    while (R > 1 && win_f(R, L0, m1) > W) --R;
+    return R;
+}
 // cursor after the first x candidates of the window (0 < x <= total)
-template <int RMAX = TCK_WR>
+template <int RMAX>
 __device__ __forceinline__ void win_advance(int n, int u0, int v0, int x, int* nu, int* nv) {
     const int R = win_rows<RMAX>(n, u0), L0 = n - v0, m1 = n - 1 - u0;
     if (x >= win_f(R, L0, m1)) {
@@ -154,9 +168,8 @@ __device__ __forceinline__ void next_pair(int n, int r, int s, int* nu, int* nv)
     else { *nu = 0; *nv = 1; }
 }
 
-__device__ __forceinline__ int rej_bound(const Sched& sch, uint64_t k) {
-    return __float2int_ru(fminf(38.5f * temp32(sch, k), 2.0e9f));
-}
+__device__ __forceinline__ int rej_of(float T32) { return __float2int_ru(fminf(38.5f * T32, 2.0e9f)); }
+__device__ __forceinline__ int rej_bound(const Sched& sch, uint64_t k) { return rej_of(temp32(sch, k)); }
 
 // θ = -T_k ln r_k in float and its margin (chain.cuh prepare_theta)
 __device__ __forceinline__ void theta_of(const Sched& sch, uint64_t seed, uint32_t chain, uint64_t kk,
@@ -201,7 +214,6 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
     uint64_t* mbar_g = reinterpret_cast<uint64_t*>(smem + L.misc + 8);    // init only
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.misc + 16);
     const bool lanew = warp < 4;                 // lane warp (else helper)
-    uint32_t* tile = reinterpret_cast<uint32_t*>(smem + L.tile) + (warp & 3) * 4 * 32 * TCK_TILE;
     const uint32_t quad_lane = (uint32_t)(32 * (warp & 3)) << 16;   // this warp's TMEM lane quadrant
     const int v = t & 127;                       // TMEM lane v = location v = facility v
 
@@ -270,7 +282,7 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
     tc::fence_after_sync();
     uint64_t k = cv.k0_dev ? *cv.k0_dev : a.k0, accepted = 0;
     // single chain: θ of the window from the precomputed ring (reuses the init operands' space)
-    ThetaRing TR = theta_ring(reinterpret_cast<float*>(smem + L.tmp), reinterpret_cast<uint64_t*>(smem + L.tbar),
+    ThetaRing<TH_SLOTS_TC> TR = theta_ring<TH_SLOTS_TC>(reinterpret_cast<float*>(smem + L.tmp), reinterpret_cast<uint64_t*>(smem + L.tbar),
                               a.theta, a.theta_kb, a.theta_cnt, k);
     if (RING && t == 0 && k < a.k_end) TR.start(k);
     tc::fence_before_sync();
@@ -284,8 +296,9 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
     uint64_t digest = cv.st->digest;
     int u0, v0;
     tri_pair(n, (int)(k % (uint64_t)M), &u0, &v0);
-    const int wmax = a.wmax;
-    int W = wmax;
+    // window cap: the ring (TH_SLOTS_TC blocks) keeps its prefetch ahead of a whole window
+    const int wcap = RING ? min(a.wscan, TCK_WSCAN) : a.wscan;
+    int W = wcap;
     int parity = 0;
     // certain-reject bound: δ > 38.5 T32(k) >= 38.4 T_kk gives exp(-δ/T) < 2^-54 <= r (chain.cuh);
     // rounded up to an integer, so the exact test below also sees every δ <= 38.5 T32(k)
@@ -302,11 +315,11 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
 #endif
 
     while (k < k_end) {
-        // ---------------- window: rows u0 .. u0+R-1 from the cursor (lane warps) ----------------
+        // ---------------- window: whole rows u0 .. u0+R-1 from the cursor (all warps) ----------------
         TCT_MARK(pt0, u0 + v0);
-        const int R = win_rows(n, u0), L0 = n - v0, m1 = n - 1 - u0;
+        const int L0 = n - v0, m1 = n - 1 - u0;
+        const int R = win_rows_whole(n, u0, L0, m1, W);
         int Wl = win_f(R, L0, m1);
-        if (W < Wl) Wl = W;
         {
             const uint64_t remaining = k_end - k;
             if ((uint64_t)Wl > remaining) Wl = (int)remaining;
@@ -316,53 +329,45 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
             TR.ensure(k + (uint64_t)Wl);
         }
         int4* sl = slots + parity * TCK_NW;
-        unsigned acc_mask = 0, near_mask = 0;
-        // this warp's window rows: u0 + hb .. u0 + hb + 7 (two groups of 4), hb = 8 (warp >> 2)
-        const int hb = 8 * (warp >> 2);
-        int rb[8], rf[8];                        // offset base (f_i - first_i) and first column of its rows
-        {
-            int f = hb == 0 ? 0 : win_f(hb, L0, m1);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int ii = hb + i;
-                rf[i] = ii == 0 ? v0 : u0 + ii + 1;
-                rb[i] = f - rf[i];
-                f += ii == 0 ? L0 : m1 - ii;
-            }
-        }
         int best_o = INT_MAX, best_d = 0, best_rs = 0;
-#pragma unroll
-        for (int g = 0; g < 2; ++g) {
-            const int h4 = hb + 4 * g;
-            if (!(h4 < R && rb[4 * g] + rf[4 * g] < Wl)) continue;   // warp-uniform: no candidates
-            uint32_t dd[4];
-            tc::tmem_ld4(tm + quad_lane + (uint32_t)(u0 + h4), dd);   // Δ_{u0+h4+i, v} (columns u0+h4 ..)
-            int pu[4];                           // p(row): carried to the accepted slot
-#pragma unroll
-            for (int i = 0; i < 4; ++i) pu[i] = p[min(u0 + h4 + i, n - 1)];
+        int nt_o[2] = {INT_MAX, INT_MAX}, nt_d[2] = {0, 0};   // this thread's near ties (R16): offset, decision
+        // groups of 8 rows u0 + 8g .. u0 + 8g + 7, g = warp / 4, + 2, ...: thread v reads its cells
+        // Δ_{u, v} (columns u) with one tcgen05.ld; offsets grow with the row, so a warp stops after
+        // its first group holding an accept (every later candidate comes after it)
+        const int NG = (R + 7) >> 3;
+        for (int g = warp >> 2; g < NG; g += 2) {
+            const int i0 = 8 * g;
+            int f = i0 == 0 ? 0 : win_f(i0, L0, m1);   // offset of row u0 + i0's first candidate
+            if (f >= Wl) break;                  // warp-uniform: the group starts past the window
+            uint32_t dd[8];
+            tc::tmem_ld8(tm + quad_lane + (uint32_t)(u0 + i0), dd);   // columns u0+i0 .. (< 140: inside G, unused)
             tc::tmem_wait_ld();
             if (v == pend_r || v == pend_s) {    // cells still being patched: their new values
                 const int* row = v == pend_r ? rowR : rowS;
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
-                    if (u0 + h4 + i < v) dd[i] = (uint32_t)row[u0 + h4 + i];
+                for (int i = 0; i < 8; ++i)
+                    if (u0 + i0 + i < v) dd[i] = (uint32_t)row[u0 + i0 + i];
             }
             // per candidate: exists / accepted outright (δ <= 0, R5) / needs the threshold test
             unsigned need = 0, am = 0;
+            int oo[8];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int o = rb[4 * g + i] + v;
+            for (int i = 0; i < 8; ++i) {
+                const int ii = i0 + i;
+                const int first = ii == 0 ? v0 : u0 + ii + 1;
+                oo[i] = f - first + v;
+                f += ii == 0 ? L0 : m1 - ii;
                 const int d = (int)dd[i];
-                const bool ex = h4 + i < R && v >= rf[4 * g + i] && vin && o < Wl;
+                const bool ex = ii < R && v >= first && vin && oo[i] < Wl;
                 am |= (unsigned)(ex && d <= 0) << i;
                 need |= (unsigned)(ex && d > 0 && d <= rejI) << i;   // above rejI: certain reject
             }
             if (__any_sync(0xffffffffu, need != 0)) {
                 const int pnk = pk == k ? pn : 0;
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
+                for (int i = 0; i < 8; ++i) {
                     if ((need >> i) & 1u) {
-                        const int o = rb[4 * g + i] + v;
+                        const int o = oo[i];
                         const int d = (int)dd[i];
                         float th, m;
                         if (RING) { th = TR.at(k + (uint64_t)o); m = 2e-4f * th + 2e-5f * Tw; }
@@ -373,28 +378,32 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
                         if (!ac && !(df > th + m)) {  // inside the margin: exact double test (R16)
                             const int x = tc_exact(d, k + (uint64_t)o, sch, seed, cv.chain);
                             ac = x & 1;
-                            near_mask |= (unsigned)((x >> 1) & 1) << (4 * g + i);
+                            if (x & 2) {          // near tie: logged after the decision if consumed
+                                const int e = nt_o[0] == INT_MAX ? 0 : 1;
+                                if (nt_o[e] == INT_MAX) { nt_o[e] = o; nt_d[e] = ac; }
+                                else near_record(sink, k + (uint64_t)o, ac);   // a third (never seen): logged eagerly
+                            }
                         }
                         am |= (unsigned)ac << i;
                     }
                 }
             }
-            acc_mask |= am << (4 * g);
-            // first accepted candidate of this thread (offsets grow with the row)
-#pragma unroll
-            for (int i = 3; i >= 0; --i) {
-                const bool ac = (am >> i) & 1u;
-                const bool better = ac && rb[4 * g + i] + v < best_o;
-                best_o = better ? rb[4 * g + i] + v : best_o;
-                best_d = better ? (int)dd[i] : best_d;
-                best_rs = better ? ((u0 + h4 + i) | (v << 8) | (pu[i] << 16) | (px << 24)) : best_rs;
+            if (__any_sync(0xffffffffu, am != 0)) {
+                if (am) {                        // this thread's first accepted candidate
+                    const int i = __ffs(am) - 1;
+                    const int u = u0 + i0 + i;
+                    best_o = oo[i];
+                    best_d = (int)dd[i];
+                    best_rs = u | (v << 8) | ((int)p[u] << 16) | (px << 24);
+                }
+                break;
             }
         }
         {
             const int wmin = __reduce_min_sync(0xffffffffu, best_o);
             if (best_o == wmin && (wmin != INT_MAX || lane == 0)) sl[warp] = make_int4(best_o, best_d, best_rs, 0);
         }
-        TCT_ACC(10, pt0, acc_mask);
+        TCT_ACC(10, pt0, best_o);
         tc::fence_before_sync();
         __syncthreads();
         tc::fence_after_sync();
@@ -403,21 +412,19 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
         const int j = __reduce_min_sync(0xffffffffu, tv);
         TCT_MARK(pt1, j);
         parity ^= 1;
-        const int consumed = (j == INT_MAX) ? Wl : j + 1;
-        if (near_mask) {                         // R16: log near ties of consumed iterations
+        if (nt_o[0] != INT_MAX) {                // R16: log near ties of consumed iterations
+            const int consumed = (j == INT_MAX) ? Wl : j + 1;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int o = rb[i] + v;
-                if (((near_mask >> i) & 1u) && o < consumed) {
-                    near_record(sink, k + (uint64_t)o, (acc_mask >> i) & 1u);
-                }
-            }
+            for (int e = 0; e < 2; ++e)
+                if (nt_o[e] < consumed) near_record(sink, k + (uint64_t)nt_o[e], nt_d[e] != 0);
         }
         if (j == INT_MAX) {                      // no accepted swap in the window
             TCT_ACC(1, pt0, j);
             k += (uint64_t)Wl;
-            win_advance(n, u0, v0, Wl, &u0, &v0);
-            W = min(2 * W, wmax);
+            u0 += R;                             // whole rows: the cursor moves to the next row
+            v0 = u0 + 1;
+            if (u0 >= n - 1) { u0 = 0; v0 = 1; }
+            W = min(2 * W, wcap);
             rejI = rej_bound(sch, k);
             Tw = temp32(sch, k);
             continue;
@@ -512,11 +519,8 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
             }
             int nu0, nv0;
             next_pair(n, r, s, &nu0, &nv0);
-            const int Wn = max(64, min(wmax, round_up32(8 * (j + 1))));
-            int Wln = win_total(n, nu0, nv0);
-            if (Wn < Wln) Wln = Wn;
-            if (kacc + 1 + (uint64_t)Wln > k_end) Wln = (int)(k_end - kacc - 1);
-            for (int o = v; !RING && o < Wln && o < TCK_TH; o += 128) {
+            const int Wln = (int)min((uint64_t)TCK_TH, k_end - kacc - 1);
+            for (int o = v; !RING && o < Wln; o += 128) {
                 float th, m;
                 theta_of(sch, seed, cv.chain, kacc + 1 + (uint64_t)o, &th, &m);
                 thm[o] = make_float2(th, m);
@@ -573,16 +577,12 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
         pend_s = s;
         pk = kacc + 1;
         {
-            const int Wn = max(64, min(wmax, round_up32(8 * (j + 1))));
             int nu0, nv0;
             next_pair(n, r, s, &nu0, &nv0);
-            int Wln = win_total(n, nu0, nv0);
-            if (Wn < Wln) Wln = Wn;
-            if (kacc + 1 + (uint64_t)Wln > k_end) Wln = (int)(k_end - kacc - 1);
-            pn = Wln < TCK_TH ? Wln : TCK_TH;
+            pn = (int)min((uint64_t)TCK_TH, k_end - kacc - 1);   // thresholds the helpers prepared
             u0 = nu0;
             v0 = nv0;
-            W = Wn;
+            W = max(64, min(wcap, round_up32(8 * (j + 1))));
         }
         ++accepted;
         k = kacc + 1;

@@ -6,8 +6,9 @@
 // only on the iteration index k (T_k by R1, r_k by R3), not on the state, so k_theta computes
 // every θ of a call's iteration range [kb, kb + cnt) up front across the whole GPU (about
 // 0.4 ms for 1e8 iterations) into an HBM buffer, and the chain kernel pulls 4 KB blocks of it
-// into a ring of TH_SLOTS blocks with cp.async.bulk (one elected thread, completion on one
-// mbarrier per slot), TH_SLOTS - 1 blocks ahead of the window.  The window then reads θ with one
+// into a ring of blocks with cp.async.bulk (one elected thread, completion on one mbarrier per
+// slot; TH_SLOTS = 8 for the scratch phase's short windows, TH_SLOTS_TC = 32 for the Δ engine's
+// whole-row windows of up to 7 blocks), as far ahead of the window as the ring allows.  The window then reads θ with one
 // shared-memory load per candidate instead of a Philox4x32-10 block, a logf and an expf.
 //
 // Exactness is unchanged: θ is the float value prepare_theta computes (chain.cuh), the window
@@ -25,9 +26,10 @@
 namespace qapsa {
 
 constexpr int TH_BLK = 1024;                     // θ per ring block (4 KB, one bulk copy)
-constexpr int TH_SLOTS = 8;                      // ring blocks (32 KB of shared memory)
+constexpr int TH_SLOTS = 8;                      // scratch phase: ring blocks (32 KB of shared memory)
 constexpr int TH_RING = TH_BLK * TH_SLOTS;
 constexpr int TH_RING_BYTES = TH_RING * 4;
+constexpr int TH_SLOTS_TC = 32;                  // Δ engine (windows up to 7 blocks): 128 KB
 constexpr unsigned long long TH_CHUNK = 1ull << 27;   // iterations per θ buffer fill (512 MB)
 
 // θ_k for k = kb + i, i < cnt (cnt a multiple of TH_BLK); any grid
@@ -59,63 +61,67 @@ __device__ __forceinline__ void fence_mbar_init() {
 }
 }  // namespace tc
 
-// One chain's view of the ring.  Every consumer thread keeps `ready` (blocks known complete,
-// identical in all threads: they wait in the same order); the issuing thread also keeps `issued`.
+// One chain's view of a ring of SLOTS blocks.  Every consumer thread keeps `ready` (blocks known
+// complete, identical in all threads: they wait in the same order); the issuing thread also keeps
+// `issued`.  A window of w iterations leaves SLOTS - ceil(w / TH_BLK) - 1 blocks of prefetch.
+template <int SLOTS>
 struct ThetaRing {
-    float* ring;                 // shared memory, TH_RING floats
-    uint64_t* bars;              // shared memory, TH_SLOTS mbarriers
+    static constexpr int RING = SLOTS * TH_BLK;
+    float* ring;                 // shared memory, RING floats
+    uint64_t* bars;              // shared memory, SLOTS mbarriers
     const float* src;            // θ of iterations [kb, kb + nblk TH_BLK)
     unsigned long long kb;
     long long nblk;
     long long ready;
     long long issued;
 
-    // issuing thread: blocks [issued, min(nblk, b_lo + TH_SLOTS)); the slot of block b held block
-    // b - TH_SLOTS < b_lo, whose iterations every consumer has passed (a CTA / group barrier
+    // issuing thread: blocks [issued, min(nblk, b_lo + SLOTS)); the slot of block b held block
+    // b - SLOTS < b_lo, whose iterations every consumer has passed (a CTA / group barrier
     // separates the last window that read it from this call)
     __device__ __forceinline__ void refill(unsigned long long k) {
         const long long b_lo = (long long)((k - kb) / TH_BLK);
-        const long long hi = min(nblk, b_lo + TH_SLOTS);
+        const long long hi = min(nblk, b_lo + SLOTS);
         for (; issued < hi; ++issued) {
-            const int slot = (int)(issued & (TH_SLOTS - 1));
+            const int slot = (int)(issued & (SLOTS - 1));
             tc::mbar_expect_tx(bars + slot, TH_BLK * 4);
             tc::bulk_g2s(ring + slot * TH_BLK, src + issued * TH_BLK, TH_BLK * 4, bars + slot);
         }
     }
-    // thread 0 of the chain before the kernel's first use: barriers, first TH_SLOTS blocks
+    // thread 0 of the chain before the kernel's first use: barriers, first SLOTS blocks
     // (the caller then synchronises the consumers)
     __device__ __forceinline__ void start(unsigned long long k) {
-        for (int i = 0; i < TH_SLOTS; ++i) tc::mbar_init(bars + i, 1);
+        for (int i = 0; i < SLOTS; ++i) tc::mbar_init(bars + i, 1);
         tc::fence_mbar_init();
         tc::fence_proxy_async();
         issued = 0;
         refill(k);
     }
-    // every consumer: θ of iterations < k_hi resident (block b completes phase (b / TH_SLOTS) & 1)
+    // every consumer: θ of iterations < k_hi resident (block b completes phase (b / SLOTS) & 1)
     __device__ __forceinline__ void ensure(unsigned long long k_hi) {
         const long long bh = (long long)((k_hi - 1 - kb) / TH_BLK);
         while (ready <= bh) {
-            tc::mbar_wait(bars + (int)(ready & (TH_SLOTS - 1)), (uint32_t)((ready / TH_SLOTS) & 1));
+            tc::mbar_wait(bars + (int)(ready & (SLOTS - 1)), (uint32_t)((ready / SLOTS) & 1));
             ++ready;
         }
     }
     __device__ __forceinline__ float at(unsigned long long kk) const {
-        return ring[(int)((kk - kb) & (unsigned long long)(TH_RING - 1))];
+        return ring[(int)((kk - kb) & (unsigned long long)(RING - 1))];
     }
     // issuing thread, before the CTA exits: no bulk copy may still be writing its shared memory
     __device__ __forceinline__ void drain() {
         for (long long b = ready; b < issued; ++b)
-            tc::mbar_wait(bars + (int)(b & (TH_SLOTS - 1)), (uint32_t)((b / TH_SLOTS) & 1));
+            tc::mbar_wait(bars + (int)(b & (SLOTS - 1)), (uint32_t)((b / SLOTS) & 1));
     }
 };
 
-__device__ __forceinline__ ThetaRing theta_ring(float* ring, uint64_t* bars, const float* src,
+template <int SLOTS>
+__device__ __forceinline__ ThetaRing<SLOTS> theta_ring(float* ring, uint64_t* bars, const float* src,
                                                 unsigned long long kb, unsigned long long cnt,
                                                 unsigned long long k) {
     // blocks are counted from the one holding k (a kernel chained after the scratch phase starts
     // inside the buffer): every slot's first use is then phase 0 of its mbarrier
     const unsigned long long b0 = (k - kb) / TH_BLK;
-    ThetaRing R;
+    ThetaRing<SLOTS> R;
     R.ring = ring;
     R.bars = bars;
     R.src = src + b0 * TH_BLK;

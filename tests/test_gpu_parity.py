@@ -190,7 +190,7 @@ def test_tmem_engine_full_range_values(n, seed):
 
 
 @pytest.mark.parametrize("scratch", [1, 0])
-@pytest.mark.parametrize("wmax", [32, 64, 256, 1024])
+@pytest.mark.parametrize("wmax", [32, 64, 256, 1024, 4096, 8192])
 def test_tmem_window_invariance(wmax, scratch):
     A, B = taixxa(100, 77)
     p0 = start_perm(100, 5, 0)

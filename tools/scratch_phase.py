@@ -35,7 +35,9 @@ L.qapsa_debug_phase_cycles(buf)
 na = max(1, buf[127])
 print(f"{ms*1e-3*1.965e9/na:.0f} clk per accept ({na} accepts in the first kernel)")
 names = ["window values ready", "tests done (from loop top)", "stage done (from decision)",
-         "staging barrier passed (from decision)", "non-accepting windows (total)"]
+         "staging barrier passed (from decision)", "non-accepting windows (total)", "accept read (from decision)",
+         "next rows' p (from decision)", "previous MMA waited (from decision)", "tensor loads done (from decision)",
+         "shared loads done (from decision)", "decision (from loop top)"]
 for w in (0,):
     b = buf[16 * w: 16 * w + 12]
-    print(f"warp {w}: " + ", ".join(f"{nm} {b[i]/na:.0f}" for i, nm in enumerate(names) if b[i]))
+    print(f"warp {w}:\n  " + "\n  ".join(f"{nm} {b[i]/na:.0f}" for i, nm in enumerate(names) if b[i]))
