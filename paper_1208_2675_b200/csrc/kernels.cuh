@@ -232,9 +232,11 @@ struct ChainArgs {
     uint32_t chain;          // Philox chain id (R3) of the chain (of CTA 0 when ens)
     unsigned long long switch_gap;   // scratch phase: switch to Δ after this many iterations
                                      // without an accept (0 = TCS_SWITCH_GAP)
-    // single-chain launches of the tensor-memory kernels: θ of iterations [theta_kb, theta_kb +
-    // theta_cnt) precomputed by k_theta (theta_ring.cuh); ensemble launches compute θ in the kernel
-    const float* theta;
+    // single-chain launches of the tensor-memory kernels: integer thresholds of iterations
+    // [theta_kb, theta_kb + theta_cnt) and their block headers precomputed by k_theta
+    // (theta_ring.cuh, R23); ensemble launches compute θ in the kernel
+    const int* theta;
+    const int4* theta_hdr;
     unsigned long long theta_kb, theta_cnt;
 };
 

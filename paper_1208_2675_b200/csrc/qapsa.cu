@@ -72,8 +72,10 @@ struct qap_ctx {
     uint8_t* dcls = nullptr;            // n
     uint16_t* dpt = nullptr;            // ncls x (n+1)
     int32_t* dD2 = nullptr;             // quad layout, same size as dD
-    // thresholds θ of a single-chain call's iterations (k_theta, theta_ring.cuh), grown on demand
-    float* dtheta = nullptr;
+    // integer thresholds of a single-chain call's iterations and their block headers (k_theta,
+    // theta_ring.cuh), grown on demand
+    int* dtheta = nullptr;
+    int4* dtheta_hdr = nullptr;
     size_t theta_cap = 0;
     // near-tie log of the last qap_ensemble_run: (chain, k, decision), R16
     unsigned int* ens_near_count = nullptr;
@@ -269,7 +271,7 @@ void qap_destroy(qap_ctx* c) {
                     c->dnear_k, c->dnear_dec, c->dscratch, c->ens_p0, c->ens_res, c->ens_best,
                     c->ens_counter, c->dkout, c->dcls, c->dpt, c->dD2, c->tp, c->tbp, c->tD,
                     c->tst, c->tkout, c->ens_near_count, c->ens_near_k, c->ens_near_dec,
-                    c->ens_near_chain, c->dtheta};
+                    c->ens_near_chain, c->dtheta, c->dtheta_hdr};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->ev0) cudaEventDestroy(c->ev0);
@@ -546,15 +548,19 @@ qap_status qap_sa_run(qap_ctx* c, uint64_t k0, uint64_t iters, const qap_schedul
     a.wscan = c->wmax ? c->wmax : TCK_WSCAN;
     a.k0 = k0; a.k_end = k0 + iters; a.seed = seed; a.sch = sch;
 
-    a.theta = nullptr;
+    a.theta = nullptr; a.theta_hdr = nullptr;
     a.theta_kb = a.theta_cnt = 0;
     if (tc) {   // θ buffer of one chunk of the call (theta_ring.cuh)
         const size_t need = (size_t)((std::min<uint64_t>(iters, TH_CHUNK) + TH_BLK - 1) / TH_BLK) * TH_BLK;
         if (c->theta_cap < need) {
             if (c->dtheta) cudaFree(c->dtheta);
+            if (c->dtheta_hdr) cudaFree(c->dtheta_hdr);
             c->dtheta = nullptr;
+            c->dtheta_hdr = nullptr;
             c->theta_cap = 0;
-            if (cudaMalloc(&c->dtheta, need * 4) != cudaSuccess) return fail(c, QAP_E_NOMEM, "θ buffer");
+            if (cudaMalloc(&c->dtheta, need * 4) != cudaSuccess ||
+                cudaMalloc(&c->dtheta_hdr, need / TH_BLK * sizeof(int4)) != cudaSuccess)
+                return fail(c, QAP_E_NOMEM, "threshold buffer");
             c->theta_cap = need;
         }
     }
@@ -580,11 +586,12 @@ qap_status qap_sa_run(qap_ctx* c, uint64_t k0, uint64_t iters, const qap_schedul
         for (uint64_t kc = k0; kc < k0 + iters; kc += TH_CHUNK) {
             const uint64_t ke = std::min<uint64_t>(k0 + iters, kc + TH_CHUNK);
             const uint64_t cnt = (ke - kc + TH_BLK - 1) / TH_BLK * TH_BLK;
-            k_theta<<<c->num_sms * 4, 256, 0, c->stream>>>(sch, seed, 0u, kc, cnt, c->dtheta);
+            k_theta<<<c->num_sms * 8, 256, 0, c->stream>>>(sch, seed, 0u, kc, cnt, c->dtheta, c->dtheta_hdr);
             CU(cudaGetLastError());
             a.k0 = kc;
             a.k_end = ke;
             a.theta = c->dtheta;
+            a.theta_hdr = c->dtheta_hdr;
             a.theta_kb = kc;
             a.theta_cnt = cnt;
             a.k0_dev = nullptr;
@@ -819,7 +826,7 @@ static qap_status ensemble_tc(qap_ctx* c, uint32_t chain_begin, uint32_t chain_c
     a.k0 = 0; a.k_end = iters; a.seed = seed; a.sch = sch;
     a.k0_dev = nullptr; a.proposal = 0;
     a.ens = 1; a.dstride = dstride; a.chain = chain_begin;
-    a.theta = nullptr; a.theta_kb = a.theta_cnt = 0;
+    a.theta = nullptr; a.theta_hdr = nullptr; a.theta_kb = a.theta_cnt = 0;
     // two scratch-phase chains share an SM but the Δ engine holds one: stay longer in the scratch
     // phase (config 5: gap 4096 / 16384 / 65536 / never = 3.67 / 3.64 / 3.62 / 3.66 s)
     a.switch_gap = 65536;

@@ -40,7 +40,7 @@ template <bool ENS> __host__ __device__ constexpr uint32_t tcs_cols() { return E
 constexpr uint64_t TCS_SWITCH_GAP = 4096;   // switch to the Δ engine after this many iterations without an accept
 
 struct ScLayout {
-    int a, b, rg, la, tmp, p, bestp, dg, xch, slots, rec, misc, tbar, bytes;
+    int a, b, rg, la, tmp, p, bestp, dg, xch, slots, rec, misc, tbar, thdr, bytes;
 };
 __host__ __device__ inline ScLayout sc_layout(int ld) {
     ScLayout L;
@@ -58,9 +58,28 @@ __host__ __device__ inline ScLayout sc_layout(int ld) {
     L.slots = o; o += 2 * TCS_RW * 16;
     L.rec = o;   o += 32;                       // the accept for the helpers, double-buffered
     L.misc = o;  o += 64;                       // mbarrier | TMEM base
-    L.tbar = o;  o += TH_SLOTS * 8;             // θ ring mbarriers
+    L.tbar = o;  o += TH_SLOTS * 8;             // threshold ring mbarriers
+    L.thdr = o;  o += TH_SLOTS * 16;            // threshold ring block headers
     L.bytes = o;
     return L;
+}
+
+// Window geometry of this row warp (rows h2, h2 + 1 of the window at cursor (u0, v0), at most W
+// candidates and rem iterations): rf = first column of the row (n if the row is not in the window),
+// rb = offset base (candidate (u0 + i, v) has offset rb + v), Wl = candidates in the window.
+struct ScWin { int Wl; int rb[2]; int rf[2]; };
+__device__ __forceinline__ ScWin sc_win(int n, int u0, int v0, int W, uint32_t rem, int h2) {
+    const int R = win_rows<4>(n, u0), L0 = n - v0, m1 = n - 1 - u0;
+    ScWin w;
+    w.Wl = min(win_f(R, L0, m1), W);
+    if ((uint32_t)w.Wl > rem) w.Wl = (int)rem;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        const int i = h2 + e;
+        w.rf[e] = i >= R ? n : i == 0 ? v0 : u0 + i + 1;
+        w.rb[e] = (i == 0 ? 0 : win_f(i, L0, m1)) - w.rf[e];
+    }
+    return w;
 }
 
 template <int NFIX, bool ENS = false>
@@ -148,8 +167,9 @@ __global__ void __launch_bounds__(TCS_NT, ENS ? 2 : 1) k_sa_scratch(const ChainA
     uint32_t ph = 1;
     tc::fence_after_sync();
     // single chain: θ of the window from the precomputed ring (reuses the init operands' space)
-    ThetaRing<TH_SLOTS> TR = theta_ring<TH_SLOTS>(reinterpret_cast<float*>(smem + L.tmp), reinterpret_cast<uint64_t*>(smem + L.tbar),
-                              a.theta, a.theta_kb, a.theta_cnt, a.k0);
+    ThetaRing<TH_SLOTS> TR = theta_ring<TH_SLOTS>(
+        reinterpret_cast<int*>(smem + L.tmp), reinterpret_cast<int4*>(smem + L.thdr),
+        reinterpret_cast<uint64_t*>(smem + L.tbar), a.theta, a.theta_hdr, a.theta_kb, a.theta_cnt, a.k0);
     if (RING && t == 0 && a.k0 < a.k_end) TR.start(a.k0);
     __syncthreads();
 
@@ -158,51 +178,45 @@ __global__ void __launch_bounds__(TCS_NT, ENS ? 2 : 1) k_sa_scratch(const ChainA
     const NearSink sink = cv.sink;
     int64_t cost = cv.st->cost, best = cv.st->best_cost;
     uint64_t digest = cv.st->digest;
-    uint64_t k = a.k0, accepted = 0, k_last = a.k0;
+    // iterations relative to k0 in 32 bits: this launch runs at most 2^31 - 1 of them (the caller
+    // continues from the iteration reached, so the trajectory does not depend on the split)
+    const uint64_t k0 = a.k0;
+    const uint32_t kr_end = (uint32_t)min((unsigned long long)(a.k_end - k0), 0x7FFFFFFFull);
+    uint32_t kr = 0, kr_last = 0;
+    uint64_t accepted = 0;
     int u0, v0;
-    tri_pair(n, (int)(k % (uint64_t)M), &u0, &v0);
+    tri_pair(n, (int)(k0 % (uint64_t)M), &u0, &v0);
     const int wmax = a.wmax;
     int W = wmax;
     int parity = 0;
-    float Tw = temp32(sch, k);                   // T at the window's first iteration (ring margin)
-    int rejI = rej_of(Tw);
+    int rejI = rej_bound(sch, k0);
     const uint32_t id_gh = tc::idesc_i8(128, 256, true);
+    const int kofs0 = RING ? (int)(k0 - TR.kb) : 0;   // ring offset of iteration k0
 #ifdef QAPSA_PHASE_TIMERS
     long long tacc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 #endif
 
   if (roww) {
-    const uint64_t gap = a.switch_gap ? a.switch_gap : TCS_SWITCH_GAP;
+    const uint32_t gap = a.switch_gap ? (uint32_t)min(a.switch_gap, (unsigned long long)0x7FFFFFFF) : (uint32_t)TCS_SWITCH_GAP;
     // The window's rows u_i = u0 + i, i < 4; this warp's are i = h2 + e, e < 2: pu[e] = p(u_i),
     // gv[e] = G[v][p(u_i)] (registers) and xch[i][v] = G_{u_i, v} (shared memory).  After an
     // accept they are produced by the stage from the PRE-update tensor memory plus the exact rank-1
     // change of the accept, so the next window is tested while the tensor cores apply that change
     // (the MMA is waited for only before the next read or write of tensor memory); after a window
-    // without accept they are read afresh.
+    // without accept they are read afresh.  The window's geometry (ScWin) is likewise computed by
+    // the stage for the next window.
     bool fresh = true;
     bool mma_pending = false;
     int pu[2];
     uint32_t gv[2];
-    while (k < k_end && k - k_last < gap) {
+    ScWin wg = sc_win(n, u0, v0, W, kr_end - kr, h2);
+    while (kr < kr_end && kr - kr_last < gap) {
         // ---------------- window: rows u0 .. u0+R-1 (R <= 4) ----------------
         TCT_MARK(pt0, u0 + v0);
-        const int R = win_rows<4>(n, u0), L0 = n - v0, m1 = n - 1 - u0;
-        int Wl = win_f(R, L0, m1);
-        if (W < Wl) Wl = W;
-        {
-            const uint64_t remaining = k_end - k;
-            if ((uint64_t)Wl > remaining) Wl = (int)remaining;
-        }
+        const int Wl = wg.Wl;
         if (RING) {
-            if (t == 0) TR.refill(k);
-            TR.ensure(k + (uint64_t)Wl);
-        }
-        int rb[2], rf[2];                        // offset base and first column of rows h2, h2 + 1
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-            const int i = h2 + e;
-            rf[e] = i == 0 ? v0 : u0 + i + 1;
-            rb[e] = (i == 0 ? 0 : win_f(i, L0, m1)) - rf[e];
+            if (t == 0) TR.refill(k0 + kr);
+            TR.ensure_ofs(kofs0 + (int)kr + Wl);
         }
         if (fresh) {
             if (mma_pending) {                   // G, H complete before they are read
@@ -239,44 +253,30 @@ __global__ void __launch_bounds__(TCS_NT, ENS ? 2 : 1) k_sa_scratch(const ChainA
             const int guv = xch[i * 128 + v];                   // G_uv = (A B'^T)[u][v]
             const int auv = As[u * ld + v], buv = Bs[pu[e] * ld + px];
             dd[e] = 2 * (guv + (int)gv[e] - Dg[u] - dv + 2 * auv * buv);   // δ(u, v) (R10d)
-            const int o = rb[e] + v;
-            const bool ex = i < R && v >= rf[e] && vin && o < Wl;
-            acc_mask |= (unsigned)(ex && dd[e] <= 0) << e;      // δ <= 0 (R5)
-            need |= (unsigned)(ex && dd[e] > 0 && dd[e] <= rejI) << e;
+            const int o = wg.rb[e] + v;
+            const bool ex = vin && v >= wg.rf[e] && o < Wl;     // (rows i >= R have rf = n)
+            if (RING) {
+                // exact integer threshold (R23): accept iff δ <= thr; a flagged iteration (thr < 0)
+                // takes the general test below
+                const int thr = TR.at_ofs(kofs0 + (int)kr + o);
+                acc_mask |= (unsigned)(ex && (dd[e] <= thr || (thr < 0 && dd[e] <= 0))) << e;   // (R5)
+                need |= (unsigned)(ex && thr < 0 && dd[e] > 0) << e;
+            } else {
+                acc_mask |= (unsigned)(ex && dd[e] <= 0) << e;      // δ <= 0 (R5)
+                need |= (unsigned)(ex && dd[e] > 0 && dd[e] <= rejI) << e;
+            }
         }
-        if (RING) {                              // branch-free θ test; the exact path only inside the margin
-            unsigned band = 0;
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int o = rb[e] + v;
-                const float th = TR.at(k + (uint64_t)max(o, 0));
-                const float m = 2e-4f * th + 2e-5f * Tw;
-                const float df = (float)dd[e];
-                const bool nd = (need >> e) & 1u;
-                acc_mask |= (unsigned)(nd && df < th - m) << e;
-                band |= (unsigned)(nd && !(df < th - m) && !(df > th + m)) << e;
-            }
-            if (__any_sync(0xffffffffu, band != 0)) {
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    if ((band >> e) & 1u) {      // inside the margin: exact double test (R16)
-                        const int x = tc_exact(dd[e], k + (uint64_t)(rb[e] + v), sch, seed, cv.chain);
-                        acc_mask |= (unsigned)(x & 1) << e;
-                        near_mask |= (unsigned)((x >> 1) & 1) << e;
-                    }
-                }
-            }
-        } else if (__any_sync(0xffffffffu, need != 0)) {
+        if (__any_sync(0xffffffffu, need != 0)) {   // general test: float θ, exact inside its margin
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 if ((need >> e) & 1u) {
-                    const int o = rb[e] + v;
+                    const uint64_t kk = k0 + kr + (uint64_t)(wg.rb[e] + v);
                     float th, m;
-                    theta_of(sch, seed, cv.chain, k + (uint64_t)o, &th, &m);
+                    theta_of(sch, seed, cv.chain, kk, &th, &m);
                     const float df = (float)dd[e];
                     bool ac = df < th - m;
                     if (!ac && !(df > th + m)) {  // inside the margin: exact double test (R16)
-                        const int x = tc_exact(dd[e], k + (uint64_t)o, sch, seed, cv.chain);
+                        const int x = tc_exact(dd[e], kk, sch, seed, cv.chain);
                         ac = x & 1;
                         near_mask |= (unsigned)((x >> 1) & 1) << e;
                     }
@@ -284,12 +284,13 @@ __global__ void __launch_bounds__(TCS_NT, ENS ? 2 : 1) k_sa_scratch(const ChainA
                 }
             }
         }
-        {   // this thread's first accepted candidate (row h2 before row h2 + 1)
-            const int e = (acc_mask & 1u) ? 0 : 1;
-            const int best_o = acc_mask ? rb[e] + v : INT_MAX;
+        {   // this thread's first accepted candidate (row h2 before row h2 + 1; selects, no indexing)
+            const bool a0 = acc_mask & 1u;
+            const int best_o = a0 ? wg.rb[0] + v : (acc_mask ? wg.rb[1] + v : INT_MAX);
+            const int bd = a0 ? dd[0] : dd[1];
+            const int brs = (u0 + h2 + (a0 ? 0 : 1)) | (v << 8) | ((a0 ? pu[0] : pu[1]) << 16) | (px << 24);
             const int wmin = __reduce_min_sync(0xffffffffu, best_o);
-            if (best_o == wmin && (wmin != INT_MAX || lane == 0))
-                sl[warp] = make_int4(best_o, dd[e], (u0 + h2 + e) | (v << 8) | (pu[e] << 16) | (px << 24), 0);
+            if (best_o == wmin && (wmin != INT_MAX || lane == 0)) sl[warp] = make_int4(best_o, bd, brs, 0);
         }
         TCT_ACC(1, pt0, acc_mask);
         group_sync(4, 32 * TCS_RW);              // window decision
@@ -302,17 +303,18 @@ __global__ void __launch_bounds__(TCS_NT, ENS ? 2 : 1) k_sa_scratch(const ChainA
             const int consumed = (j == INT_MAX) ? Wl : j + 1;
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-                const int o = rb[e] + v;
-                if (((near_mask >> e) & 1u) && o < consumed) near_record(sink, k + (uint64_t)o, (acc_mask >> e) & 1u);
+                const int o = wg.rb[e] + v;
+                if (((near_mask >> e) & 1u) && o < consumed)
+                    near_record(sink, k0 + kr + (uint64_t)o, (acc_mask >> e) & 1u);
             }
         }
         if (j == INT_MAX) {
             TCT_ACC(4, pt0, j);
-            k += (uint64_t)Wl;
+            kr += (uint32_t)Wl;
             win_advance<4>(n, u0, v0, Wl, &u0, &v0);
             W = min(2 * W, wmax);
-            Tw = temp32(sch, k);
-            rejI = rej_of(Tw);
+            wg = sc_win(n, u0, v0, W, kr_end - kr, h2);
+            if (!RING) rejI = rej_bound(sch, k0 + kr);   // (the ring path needs no certain-reject bound)
             fresh = true;
             continue;
         }
@@ -321,7 +323,7 @@ __global__ void __launch_bounds__(TCS_NT, ENS ? 2 : 1) k_sa_scratch(const ChainA
         const int dw = win.y;
         const int r = win.z & 0xFF, s = (win.z >> 8) & 0xFF;
         const int pr = (win.z >> 16) & 0xFF, ps = (int)((unsigned)win.z >> 24);
-        const uint64_t kacc = k + (uint64_t)j;
+        const uint32_t kracc = kr + (uint32_t)j;
         TCT_ACC(5, pt1, r + ps);
         // ---------------- stage: the G|H update operands, D'', the next window's rows ----------------
         int nu0, nv0;                            // next window: cursor after (r, s)
@@ -330,7 +332,8 @@ __global__ void __launch_bounds__(TCS_NT, ENS ? 2 : 1) k_sa_scratch(const ChainA
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
             nu[e] = min(nu0 + h2 + e, n - 1);
-            npu[e] = nu[e] == r ? ps : nu[e] == s ? pr : (int)p[nu[e]];
+            const int pn = p[nu[e]];             // unconditional load, then the swap's correction
+            npu[e] = nu[e] == r ? ps : nu[e] == s ? pr : pn;
         }
         TCT_ACC(6, pt1, npu[0] + npu[1]);
         if (mma_pending) {                       // the previous update complete: tensor memory is current
@@ -349,12 +352,10 @@ __global__ void __launch_bounds__(TCS_NT, ENS ? 2 : 1) k_sa_scratch(const ChainA
             tc::tmem_ld1(tm + quad_lane + TCS_COL_G + (uint32_t)npu[e], g4[e]);
             tc::tmem_ld1(tm + quad_lane + TCS_COL_H + (uint32_t)nu[e], h4[e]);
         }
-        int arv = 0, asv = 0, bfr = 0, bfs = 0;
-        if (vin) {
-            arv = As[r * ld + v]; asv = As[s * ld + v];
-            bfr = Bs[pr * ld + v]; bfs = Bs[ps * ld + v];
-        }
-        const int dA = arv - asv, dBf = bfr - bfs;
+        // (v >= n reads padding or the next row: in bounds, and those lanes' values are never used)
+        const int arv = As[r * ld + v], asv = As[s * ld + v];
+        const int bfr = Bs[pr * ld + v], bfs = Bs[ps * ld + v];
+        const int dA = vin ? arv - asv : 0, dBf = vin ? bfr - bfs : 0;
         int dAu[2], dBfu[2];                     // dA of the next rows (locations), dBf of their facilities
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
@@ -369,15 +370,16 @@ __global__ void __launch_bounds__(TCS_NT, ENS ? 2 : 1) k_sa_scratch(const ChainA
             *reinterpret_cast<uint32_t*>(Rg + 4096 + ro) = b8(dA) << 8;    // H rows: location v
         }
         const int Wn = max(64, min(wmax, round_up32(8 * (j + 1))));
+        const ScWin wn = sc_win(n, nu0, nv0, Wn, kr_end - kracc - 1, h2);   // next window's geometry
         if (t == 0) {                            // the accept, for the helper warp (buffer by accept parity:
-            int* rc = rec + 4 * (int)(accepted & 1);   // the helper is at most one accept behind)
+            const uint64_t kacc = k0 + kracc;    // the helper is at most one accept behind)
+            int* rc = rec + 4 * (int)(accepted & 1);
             rc[0] = r; rc[1] = s;
             rc[2] = (int)(uint32_t)kacc; rc[3] = (int)(uint32_t)(kacc >> 32);
         }
         TCT_ACC(9, pt1, dAu[1] + dBfu[1] + arv + bfs);
         if (h2 == 0) {                           // D'' (one thread per v)
-            int dB = 0;
-            if (vin) dB = (int)Bs[pr * ld + px] - (int)Bs[ps * ld + px];
+            const int dB = vin ? (int)Bs[pr * ld + px] - (int)Bs[ps * ld + px] : 0;
             const int ars = As[r * ld + s], brs = Bs[pr * ld + ps];
             tc::tmem_wait_ld();
             const int dnew = (v == r) ? (int)gps + ars * brs : (v == s) ? (int)gpr + ars * brs : dv - dA * dB;
@@ -398,8 +400,10 @@ __global__ void __launch_bounds__(TCS_NT, ENS ? 2 : 1) k_sa_scratch(const ChainA
             if (vin) xch[(h2 + e) * 128 + qv] = (int)h4[e] - dBf * dAu[e];  // H''[v][u_i] = G''_{u_i, p''^-1(v)}
         }
         TCT_ACC(2, pt1, gv[1]);
-        if (h2 == 0 && !ENS) tc::tmem_wait_st();
-        tc::fence_proxy_async();
+        if (h2 == 0) {                           // the update's operands visible to the tensor cores
+            if (!ENS) tc::tmem_wait_st();
+            tc::fence_proxy_async();
+        }
         tc::fence_before_sync();
         group_sync(1, TCS_NT);                   // operands staged, next rows exchanged: MMA issue
         TCT_ACC(3, pt1, xch[v]);
@@ -413,11 +417,11 @@ __global__ void __launch_bounds__(TCS_NT, ENS ? 2 : 1) k_sa_scratch(const ChainA
         u0 = nu0;
         v0 = nv0;
         W = Wn;
+        wg = wn;
         ++accepted;
-        k = kacc + 1;
-        k_last = k;
-        Tw = temp32(sch, k);
-        rejI = rej_of(Tw);
+        kr = kracc + 1;
+        kr_last = kr;
+        if (!RING) rejI = rej_bound(sch, k0 + kr);
     }
     if (mma_pending) {                           // the last update complete before tensor memory is freed
         tc::mbar_wait(mbar, ph);
@@ -466,7 +470,7 @@ __global__ void __launch_bounds__(TCS_NT, ENS ? 2 : 1) k_sa_scratch(const ChainA
         cv.st->best_cost = best;
         cv.st->accepted += accepted;
         unsigned long long* ko = k_out + (ENS ? 2 * blockIdx.x : 0);
-        ko[0] = k;                               // iteration reached (the Δ engine starts here)
+        ko[0] = k0 + kr;                         // iteration reached (the Δ engine starts here)
         ko[1] = accepted;                        // swaps accepted in this phase
     }
     if (t == 32 * TCS_RW) cv.st->digest = digest;    // helper lane 0 holds the digest

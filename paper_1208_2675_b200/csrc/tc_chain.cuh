@@ -70,7 +70,7 @@ __host__ __device__ __forceinline__ int cofs(int x, int k) {
 }
 
 struct TcLayout {
-    int a, b, rd, rg, rh, tmp, p, pinv, bestp, rowr, rows, xbuf, zbuf, slots, thm, misc, tbar, bytes;
+    int a, b, rd, rg, rh, tmp, p, pinv, bestp, rowr, rows, xbuf, zbuf, slots, thm, misc, tbar, thdr, bytes;
 };
 // ld: row stride of A and B (row_stride(n, true) <= 144)
 __host__ __device__ inline TcLayout tc_layout(int ld) {
@@ -93,7 +93,8 @@ __host__ __device__ inline TcLayout tc_layout(int ld) {
     L.slots = o; o += 2 * TCK_NW * 16;
     L.thm = o;   o += TCK_TH * 8;               // (θ, margin) by window offset
     L.misc = o;  o += 64;                       // mbarriers (2 x 8 B) | TMEM base (4 B)
-    L.tbar = o;  o += TH_SLOTS_TC * 8;          // θ ring mbarriers
+    L.tbar = o;  o += TH_SLOTS_TC * 8;          // threshold ring mbarriers
+    L.thdr = o;  o += TH_SLOTS_TC * 16;         // threshold ring block headers
     L.bytes = o;
     return L;
 }
@@ -282,8 +283,9 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
     tc::fence_after_sync();
     uint64_t k = cv.k0_dev ? *cv.k0_dev : a.k0, accepted = 0;
     // single chain: θ of the window from the precomputed ring (reuses the init operands' space)
-    ThetaRing<TH_SLOTS_TC> TR = theta_ring<TH_SLOTS_TC>(reinterpret_cast<float*>(smem + L.tmp), reinterpret_cast<uint64_t*>(smem + L.tbar),
-                              a.theta, a.theta_kb, a.theta_cnt, k);
+    ThetaRing<TH_SLOTS_TC> TR = theta_ring<TH_SLOTS_TC>(
+        reinterpret_cast<int*>(smem + L.tmp), reinterpret_cast<int4*>(smem + L.thdr),
+        reinterpret_cast<uint64_t*>(smem + L.tbar), a.theta, a.theta_hdr, a.theta_kb, a.theta_cnt, k);
     if (RING && t == 0 && k < a.k_end) TR.start(k);
     tc::fence_before_sync();
     __syncthreads();
@@ -303,7 +305,6 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
     // certain-reject bound: δ > 38.5 T32(k) >= 38.4 T_kk gives exp(-δ/T) < 2^-54 <= r (chain.cuh);
     // rounded up to an integer, so the exact test below also sees every δ <= 38.5 T32(k)
     int rejI = rej_bound(sch, k);
-    float Tw = temp32(sch, k);                   // T at the window's first iteration (ring margin)
     uint64_t pk = ~0ull;                         // window whose thresholds are in thm
     int pn = 0;                                  // ... for offsets [0, pn)
     int pend_r = -1, pend_s = -1;                // rows r, s whose TMEM cells (lane r|s, column < r|s)
@@ -335,6 +336,55 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
         // Δ_{u, v} (columns u) with one tcgen05.ld; offsets grow with the row, so a warp stops after
         // its first group holding an accept (every later candidate comes after it)
         const int NG = (R + 7) >> 3;
+        // exact integer thresholds (R23) unless a block of the window is flagged or the window is
+        // cut short by the end of the call: the general path below
+        const int2 sp = RING ? TR.span(k, k + (uint64_t)Wl) : make_int2(1, 0);
+        if (!sp.x && Wl == win_f(R, L0, m1)) {
+            // thread v's candidates: rows [ulo, uhi] (row u0 from column v0 on, u < v)
+            const int ulo = v >= v0 ? u0 : u0 + 1;
+            const int uhi = vin ? min(v - 1, u0 + R - 1) : -1;
+            const int kofs = (int)(k - TR.kb);
+            for (int g = warp >> 2; g < NG; g += 2) {
+                const int i0 = 8 * g;
+                int f = i0 == 0 ? 0 : win_f(i0, L0, m1);   // offset of row u0 + i0's first candidate
+                uint32_t dd[8];
+                tc::tmem_ld8(tm + quad_lane + (uint32_t)(u0 + i0), dd);
+                const int lo = ulo - u0 - i0, hi = uhi - u0 - i0;   // this thread's rows i in [lo, hi]
+                tc::tmem_wait_ld();
+                if (v == pend_r || v == pend_s) {    // cells still being patched: their new values
+                    const int* row = v == pend_r ? rowR : rowS;
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+                        if (u0 + i0 + i < v) dd[i] = (uint32_t)row[u0 + i0 + i];
+                }
+                int mn = INT_MAX;                // smallest δ of the thread's candidates
+#pragma unroll
+                for (int i = 0; i < 8; ++i) mn = min(mn, (i >= lo && i <= hi) ? (int)dd[i] : INT_MAX);
+                unsigned am = 0;
+                int oo[8];
+                if (__any_sync(0xffffffffu, mn <= sp.y)) {   // else every candidate is above every threshold
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const int ii = i0 + i;
+                        const int first = ii == 0 ? v0 : u0 + ii + 1;
+                        oo[i] = f - first + v;
+                        f += ii == 0 ? L0 : m1 - ii;
+                        const int thr = TR.ring[(kofs + oo[i]) & (TR.RING - 1)];
+                        am |= (unsigned)(i >= lo && i <= hi && (int)dd[i] <= thr) << i;
+                    }
+                }
+                if (__any_sync(0xffffffffu, am != 0)) {
+                    if (am) {                    // this thread's first accepted candidate
+                        const int i = __ffs(am) - 1;
+                        const int u = u0 + i0 + i;
+                        best_o = oo[i];
+                        best_d = (int)dd[i];
+                        best_rs = u | (v << 8) | ((int)p[u] << 16) | (px << 24);
+                    }
+                    break;
+                }
+            }
+        } else
         for (int g = warp >> 2; g < NG; g += 2) {
             const int i0 = 8 * g;
             int f = i0 == 0 ? 0 : win_f(i0, L0, m1);   // offset of row u0 + i0's first candidate
@@ -370,8 +420,7 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
                         const int o = oo[i];
                         const int d = (int)dd[i];
                         float th, m;
-                        if (RING) { th = TR.at(k + (uint64_t)o); m = 2e-4f * th + 2e-5f * Tw; }
-                        else if (o < pnk) { const float2 q = thm[o]; th = q.x; m = q.y; }
+                        if (!RING && o < pnk) { const float2 q = thm[o]; th = q.x; m = q.y; }
                         else theta_of(sch, seed, cv.chain, k + (uint64_t)o, &th, &m);
                         const float df = (float)d;
                         bool ac = df < th - m;
@@ -426,7 +475,6 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
             if (u0 >= n - 1) { u0 = 0; v0 = 1; }
             W = min(2 * W, wcap);
             rejI = rej_bound(sch, k);
-            Tw = temp32(sch, k);
             continue;
         }
         const unsigned bw = __ballot_sync(0xffffffffu, tv == j);
@@ -587,7 +635,6 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
         ++accepted;
         k = kacc + 1;
         rejI = rej_bound(sch, k);
-        Tw = temp32(sch, k);
     }
     if (RING && t == 0) TR.drain();
 
