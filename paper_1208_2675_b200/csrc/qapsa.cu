@@ -844,7 +844,7 @@ static qap_status ensemble_tc(qap_ctx* c, uint32_t chain_begin, uint32_t chain_c
     // columns fill the SM's 512
     const int ssm = std::max(sc_layout(c->ld).bytes, c->smem_optin / 3 + 1024);
     CU(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, ssm));
-    ks<<<chain_count, TCS_NT, ssm, c->stream>>>(a, c->tkout);
+    ks<<<chain_count, tcs_nt<true>(), ssm, c->stream>>>(a, c->tkout);
     CU(cudaGetLastError());
     const int dt = 256, db = (c->M + dt - 1) / dt;
     for (uint32_t c0 = 0; c0 < chain_count; c0 += 65535u) {   // gridDim.y <= 65535: slices of chains

@@ -29,8 +29,13 @@
 
 namespace qapsa {
 
-constexpr int TCS_NT = 288;            // 8 row warps (two window rows each) + 1 helper warp
+constexpr int TCS_NT = 288;            // 8 row warps (two window rows each) + 1 helper warp (MMA, digest)
 constexpr int TCS_RW = 8;              // row warps
+// ensemble launches add a θ producer warp: thresholds of the chain's coming iterations into a
+// shared-memory ring (each θ computed once, instead of per candidate and window)
+constexpr int TCS_EB = 256;            // producer block (iterations)
+constexpr int TCS_ERING = 2048;        // ring (iterations, 8 blocks; windows are <= 4 rows < 1792)
+template <bool ENS> __host__ __device__ constexpr int tcs_nt() { return ENS ? TCS_NT + 32 : TCS_NT; }
 constexpr uint32_t TCS_COL_G = 0;        // G: TMEM columns [0, 128)
 constexpr uint32_t TCS_COL_H = 128;      // H: TMEM columns [128, 256)
 constexpr uint32_t TCS_COL_L = 256;      // single chain: A operand of the update [dA, -dBf] (K = 32)
@@ -40,7 +45,7 @@ template <bool ENS> __host__ __device__ constexpr uint32_t tcs_cols() { return E
 constexpr uint64_t TCS_SWITCH_GAP = 4096;   // switch to the Δ engine after this many iterations without an accept
 
 struct ScLayout {
-    int a, b, rg, la, tmp, p, bestp, dg, xch, slots, rec, misc, tbar, thdr, bytes;
+    int a, b, rg, la, tmp, p, bestp, dg, xch, slots, rec, misc, tbar, thdr, ering, ebar, ectl, bytes;
 };
 __host__ __device__ inline ScLayout sc_layout(int ld) {
     ScLayout L;
@@ -60,6 +65,9 @@ __host__ __device__ inline ScLayout sc_layout(int ld) {
     L.misc = o;  o += 64;                       // mbarrier | TMEM base
     L.tbar = o;  o += TH_SLOTS * 8;             // threshold ring mbarriers
     L.thdr = o;  o += TH_SLOTS * 16;            // threshold ring block headers
+    L.ering = o; o += TCS_ERING * 4;            // ensemble: θ ring (float) of the producer warp
+    L.ebar = o;  o += (TCS_ERING / TCS_EB) * 8; //   its block mbarriers
+    L.ectl = o;  o += 16;                       //   consumer offset, stop flag
     L.bytes = o;
     return L;
 }
@@ -83,7 +91,7 @@ __device__ __forceinline__ ScWin sc_win(int n, int u0, int v0, int W, uint32_t r
 }
 
 template <int NFIX, bool ENS = false>
-__global__ void __launch_bounds__(TCS_NT, ENS ? 2 : 1) k_sa_scratch(const ChainArgs a, unsigned long long* k_out) {
+__global__ void __launch_bounds__(tcs_nt<ENS>(), ENS ? 2 : 1) k_sa_scratch(const ChainArgs a, unsigned long long* k_out) {
     constexpr bool RING = !ENS;                  // single chain: precomputed θ (theta_ring.cuh)
     extern __shared__ __align__(16) unsigned char smem[];
     const ChainView cv = chain_view<ENS>(a);     // this CTA's chain (ensemble launches)
@@ -103,6 +111,9 @@ __global__ void __launch_bounds__(TCS_NT, ENS ? 2 : 1) k_sa_scratch(const ChainA
     int4* slots = reinterpret_cast<int4*>(smem + L.slots);
     int* rec = reinterpret_cast<int*>(smem + L.rec);
     uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + L.misc);          // G|H update done
+    float* ering = reinterpret_cast<float*>(smem + L.ering);              // ensemble θ ring
+    uint64_t* ebar = reinterpret_cast<uint64_t*>(smem + L.ebar);
+    volatile int* ectl = reinterpret_cast<volatile int*>(smem + L.ectl);  // [0] consumer offset, [1] stop
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.misc + 8);
     const bool lanew = warp < 4;                 // lane warps: thread v owns TMEM lane v (one per v)
     const bool roww = warp < TCS_RW;             // row warps: window rows 2h, 2h + 1 (h = warp / 4)
@@ -112,15 +123,21 @@ __global__ void __launch_bounds__(TCS_NT, ENS ? 2 : 1) k_sa_scratch(const ChainA
     const bool vin = v < n;
 
     // ---------------- load the chain state; G and H on the tensor cores ----------------
-    copy_words(As, a.A, n * ld, t, TCS_NT);
-    copy_words(Bs, a.B, n * ld, t, TCS_NT);
-    for (int i = t; i < n; i += TCS_NT) {
+    constexpr int NT = tcs_nt<ENS>();
+    copy_words(As, a.A, n * ld, t, NT);
+    copy_words(Bs, a.B, n * ld, t, NT);
+    for (int i = t; i < n; i += NT) {
         p[i] = (uint16_t)cv.p[i];
         best_p[i] = (uint16_t)cv.best_p[i];
     }
-    for (int i = t; i < (256 + 128) * 32 / 16; i += TCS_NT) reinterpret_cast<uint4*>(Rg)[i] = make_uint4(0, 0, 0, 0);
+    for (int i = t; i < (256 + 128) * 32 / 16; i += NT) reinterpret_cast<uint4*>(Rg)[i] = make_uint4(0, 0, 0, 0);
     if (warp == 0) tc::tmem_alloc(tmem_slot, tcs_cols<ENS>());
     if (t == 0) tc::mbar_init(mbar, 1);
+    if (ENS && t == 0) {                         // θ producer ring: block barriers, consumer offset 0, no stop
+        for (int b = 0; b < TCS_ERING / TCS_EB; ++b) tc::mbar_init(reinterpret_cast<uint64_t*>(smem + L.ebar) + b, 1);
+        reinterpret_cast<int*>(smem + L.ectl)[0] = 0;
+        reinterpret_cast<int*>(smem + L.ectl)[1] = 0;
+    }
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
@@ -133,7 +150,7 @@ __global__ void __launch_bounds__(TCS_NT, ENS ? 2 : 1) k_sa_scratch(const ChainA
     {
         uint8_t* Ac = smem + L.tmp;
         uint8_t* Cc = Ac + 128 * 128;
-        for (int idx = t; idx < 128 * 128; idx += TCS_NT) {
+        for (int idx = t; idx < 128 * 128; idx += NT) {
             const int x = idx >> 7, kk = idx & 127;
             const bool in = x < n && kk < n;
             Ac[cofs(x, kk)] = in ? As[x * ld + kk] : (uint8_t)0;
@@ -210,13 +227,35 @@ __global__ void __launch_bounds__(TCS_NT, ENS ? 2 : 1) k_sa_scratch(const ChainA
     int pu[2];
     uint32_t gv[2];
     ScWin wg = sc_win(n, u0, v0, W, kr_end - kr, h2);
+    int ring_blo = -1, ring_hi = 0;              // ring: last block refilled from, offsets known resident
+    int ering_ready = 0;                         // ensemble: producer blocks known complete
+    float Tw = 0.0f;
+    static_assert(TH_BLK == 1024, "ring_blo counts 1024-iteration blocks");
     while (kr < kr_end && kr - kr_last < gap) {
         // ---------------- window: rows u0 .. u0+R-1 (R <= 4) ----------------
         TCT_MARK(pt0, u0 + v0);
         const int Wl = wg.Wl;
         if (RING) {
-            if (t == 0) TR.refill(k0 + kr);
-            TR.ensure_ofs(kofs0 + (int)kr + Wl);
+            const int ko = kofs0 + (int)kr;
+            if (t == 0 && (ko >> 10) != ring_blo) {   // a block passed: its slot can be refilled
+                ring_blo = ko >> 10;
+                TR.refill(k0 + kr);
+            }
+            if (ko + Wl > ring_hi) {             // blocks not yet known complete
+                TR.ensure_ofs(ko + Wl);
+                ring_hi = (int)(TR.ready * TH_BLK);
+            }
+        } else {                                 // ensemble: the producer warp's ring
+            if (t == 0) *ectl = (int)kr;         // blocks below kr may be refilled
+            if ((int)kr + Wl > ring_hi) {
+                while (ering_ready * TCS_EB < (int)kr + Wl) {
+                    constexpr int NB = TCS_ERING / TCS_EB;
+                    tc::mbar_wait(ebar + (ering_ready % NB), (uint32_t)((ering_ready / NB) & 1));
+                    ++ering_ready;
+                }
+                ring_hi = ering_ready * TCS_EB;
+            }
+            Tw = temp32(sch, k0 + kr);           // T at the window's first iteration (>= T_k of the window)
         }
         if (fresh) {
             if (mma_pending) {                   // G, H complete before they are read
@@ -244,7 +283,7 @@ __global__ void __launch_bounds__(TCS_NT, ENS ? 2 : 1) k_sa_scratch(const ChainA
         int4* sl = slots + parity * TCS_RW;
         unsigned acc_mask = 0, near_mask = 0;
         const int dv = Dg[v];
-        unsigned need = 0;
+        unsigned need = 0, band = 0;
         int dd[2];
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
@@ -262,13 +301,23 @@ __global__ void __launch_bounds__(TCS_NT, ENS ? 2 : 1) k_sa_scratch(const ChainA
                 acc_mask |= (unsigned)(ex && (dd[e] <= thr || (thr < 0 && dd[e] <= 0))) << e;   // (R5)
                 need |= (unsigned)(ex && thr < 0 && dd[e] > 0) << e;
             } else {
-                acc_mask |= (unsigned)(ex && dd[e] <= 0) << e;      // δ <= 0 (R5)
-                need |= (unsigned)(ex && dd[e] > 0 && dd[e] <= rejI) << e;
+                // ensemble: θ_k from the producer's ring (prepare_theta), decided outside its margin
+                // (T = Tw >= T_k), exact double test inside it (R16); δ <= 0 accepted (R5)
+                const float th = ering[((int)kr + o) & (TCS_ERING - 1)];
+                const float m = 2e-4f * th + 2e-5f * Tw;
+                const float df = (float)dd[e];
+                acc_mask |= (unsigned)(ex && (dd[e] <= 0 || df < th - m)) << e;
+                band |= (unsigned)(ex && dd[e] > 0 && !(df < th - m) && !(df > th + m)) << e;
             }
         }
-        if (__any_sync(0xffffffffu, need != 0)) {   // general test: float θ, exact inside its margin
+        if (__any_sync(0xffffffffu, (need | band) != 0)) {   // general test: float θ, exact inside its margin
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
+                if ((band >> e) & 1u) {          // ensemble, inside the margin: exact double test (R16)
+                    const int x = tc_exact(dd[e], k0 + kr + (uint64_t)(wg.rb[e] + v), sch, seed, cv.chain);
+                    acc_mask |= (unsigned)(x & 1) << e;
+                    near_mask |= (unsigned)((x >> 1) & 1) << e;
+                }
                 if ((need >> e) & 1u) {
                     const uint64_t kk = k0 + kr + (uint64_t)(wg.rb[e] + v);
                     float th, m;
@@ -293,6 +342,8 @@ __global__ void __launch_bounds__(TCS_NT, ENS ? 2 : 1) k_sa_scratch(const ChainA
             if (best_o == wmin && (wmin != INT_MAX || lane == 0)) sl[warp] = make_int4(best_o, bd, brs, 0);
         }
         TCT_ACC(1, pt0, acc_mask);
+        // probe the previous update MMA now: the stage then waits only if it is still running
+        const bool mma_done = !mma_pending || tc::mbar_test(mbar, ph);
         group_sync(4, 32 * TCS_RW);              // window decision
         const int tv = lane < TCS_RW ? sl[lane].x : INT_MAX;
         const int j = __reduce_min_sync(0xffffffffu, tv);
@@ -337,7 +388,7 @@ __global__ void __launch_bounds__(TCS_NT, ENS ? 2 : 1) k_sa_scratch(const ChainA
         }
         TCT_ACC(6, pt1, npu[0] + npu[1]);
         if (mma_pending) {                       // the previous update complete: tensor memory is current
-            tc::mbar_wait(mbar, ph);
+            if (!mma_done) tc::mbar_wait(mbar, ph);
             ph ^= 1;
             tc::fence_after_sync();
         }
@@ -429,8 +480,32 @@ __global__ void __launch_bounds__(TCS_NT, ENS ? 2 : 1) k_sa_scratch(const ChainA
         tc::fence_after_sync();
     }
     if (RING && t == 0) TR.drain();
+    if (ENS && t == 0) ectl[1] = 1;              // release the θ producer
     if (t == 0) rec[4 * (int)(accepted & 1)] = -1;
     group_sync(1, TCS_NT);                       // release the helper
+  } else if (ENS && warp == TCS_RW + 1) {
+    // ---------------- ensemble θ producer: θ_k of the coming iterations, block by block ----------------
+    constexpr int NB = TCS_ERING / TCS_EB;
+    for (uint32_t b = 0; (uint64_t)b * TCS_EB < (uint64_t)kr_end; ++b) {
+        if (b >= (uint32_t)NB) {                 // the slot's previous block consumed?
+            const int need_off = (int)((b - NB + 1) * TCS_EB);
+            bool stop = false;
+            while (ectl[0] < need_off && !(stop = ectl[1] != 0)) __nanosleep(64);
+            if (stop) break;
+        }
+        for (int i = lane; i < TCS_EB; i += 32) {
+            Prep pr;
+            pr.k = k0 + (uint64_t)b * TCS_EB + (uint64_t)i;
+            prepare_theta(pr, sch, seed, cv.chain);
+            ering[(b * TCS_EB + i) & (TCS_ERING - 1)] = pr.th;
+        }
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence_block();
+            tc::mbar_arrive(ebar + (b % NB));
+        }
+        if (ectl[1] != 0) break;
+    }
   } else {
     // ---------------- helper warp: the update MMA of each accept, digest ----------------
     for (uint64_t na = 0;; ++na) {
@@ -461,7 +536,7 @@ __global__ void __launch_bounds__(TCS_NT, ENS ? 2 : 1) k_sa_scratch(const ChainA
     if (t == 0) { atomicAdd(&g_phase_cycles[127], accepted); }
 #endif
     __syncthreads();
-    for (int i = t; i < n; i += TCS_NT) {
+    for (int i = t; i < n; i += NT) {
         cv.p[i] = p[i];
         cv.best_p[i] = best_p[i];
     }
