@@ -616,6 +616,53 @@ def run_config4(args, Q):
 
 
 # ----------------------------------------------------------- dry run ---
+def run_sweep(args):
+    """Fig. 2 of the paper (Eq.(4)): for a BASELINE instance and I = 1e4 ... Imax, one
+    chain with an I-iteration schedule on the GPU (device time of the call, through the C-ABI) and
+    the non-parallel Delta-matrix SA of the paper's ref. [17] -- the oracle in DELTA mode, one host
+    core (the cpu_baseline role) -- on the same I; P = t_non-parallel / t_parallel.  Both sides
+    must end with the same best cost (bit-exact trajectories).  One JSON line."""
+    import torch
+    import oracle as O
+    from paper_1208_2675_b200 import qapsa as Q
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
+    A, B, p0, cfg = config(args.sweep)
+    rows = []
+    I = 10**4
+    while I <= args.sweep_imax:
+        with Q.Solver(A, B, p0) as s:
+            s.delta_init()
+            t0, tf = s.schedule_bounds()
+            s.run(0, min(I, 10**4), Q.make_schedule(Q.QAP_COOL_GEOMETRIC, t0, tf, I), SA_SEED)   # warm-up
+        with Q.Solver(A, B, p0) as s:
+            s.delta_init()
+            t0, tf = s.schedule_bounds()
+            g = s.run(0, I, Q.make_schedule(Q.QAP_COOL_GEOMETRIC, t0, tf, I), SA_SEED)
+            ms, _ = s.last_kernel_time()
+            eng = s.engine()
+        sch = O.geometric_schedule_for(A, B, p0, I)
+        run = O.Run(A, B, p0, mode=O.MODE_DELTA)
+        t = time.perf_counter()
+        st = run.run(0, I, sch, SA_SEED)
+        t_np = time.perf_counter() - t
+        row = {"I": I, "t_parallel_s": ms / 1e3, "t_non_parallel_s": t_np, "P": t_np / (ms / 1e3),
+               "accepted": g["accepted"], "best_cost": g["best_cost"],
+               "oracle_best_cost": int(st["best_cost"]), "engine": eng}
+        if row["best_cost"] != row["oracle_best_cost"]:
+            raise SystemExit(f"sweep: best cost differs from the oracle at I = {I}")
+        rows.append(row)
+        log(json.dumps(row))
+        I *= 10
+    host = host_info()
+    print(json.dumps({"sweep": "Fig. 2 / Eq.(4): P = t_non-parallel / t_parallel against I",
+                      "config": args.sweep, "instance": cfg["name"], "seed": SA_SEED,
+                      "non_parallel": "oracle DELTA mode (the non-parallel Delta-matrix SA, P:44-50), 1 host core",
+                      "parallel": "this library, 1 B200 (device time of the call, threshold precompute included)",
+                      "cpu_model": host.get("cpu_model"), "rows": rows}), flush=True)
+    return 0
+
+
 def run_dry(args):
     """Host path only (no GPU, no method arithmetic): rank environment, chain partition, the
     ensemble driver's collectives on gloo with a stub rank runner, and rank 0's JSON line."""
@@ -667,7 +714,11 @@ def main():
     ap.add_argument("--cpu-ens-chains", type=int, default=16)
     ap.add_argument("--ref-sample", type=int, default=10**7)
     ap.add_argument("--ref-chains", type=int, default=8)
+    ap.add_argument("--sweep", type=int, default=0, help="Fig. 2 sweep (Eq.(4)) on this BASELINE config")
+    ap.add_argument("--sweep-imax", type=int, default=10**8)
     args = ap.parse_args()
+    if args.sweep:
+        return run_sweep(args)
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         return self_launch(args, sys.argv[1:])
     if args.dry_run:

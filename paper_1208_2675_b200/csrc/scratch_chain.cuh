@@ -65,9 +65,9 @@ __host__ __device__ inline ScLayout sc_layout(int ld) {
     L.misc = o;  o += 64;                       // mbarrier | TMEM base
     L.tbar = o;  o += TH_SLOTS * 8;             // threshold ring mbarriers
     L.thdr = o;  o += TH_SLOTS * 16;            // threshold ring block headers
-    L.ering = o; o += TCS_ERING * 4;            // ensemble: θ ring (float) of the producer warp
-    L.ebar = o;  o += (TCS_ERING / TCS_EB) * 8; //   its block mbarriers
-    L.ectl = o;  o += 16;                       //   consumer offset, stop flag
+    L.ering = o; o += TCS_ERING * 8;            // ensemble: (θ - m, θ + m) ring (float2) of the producer warp
+    L.ebar = o;  o += (TCS_ERING / TCS_EB) * 16; //   its block mbarriers: full[NB], empty[NB]
+    L.ectl = o;  o += 16;                       //   stop flag
     L.bytes = o;
     return L;
 }
@@ -111,9 +111,9 @@ __global__ void __launch_bounds__(tcs_nt<ENS>(), ENS ? 2 : 1) k_sa_scratch(const
     int4* slots = reinterpret_cast<int4*>(smem + L.slots);
     int* rec = reinterpret_cast<int*>(smem + L.rec);
     uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + L.misc);          // G|H update done
-    float* ering = reinterpret_cast<float*>(smem + L.ering);              // ensemble θ ring
-    uint64_t* ebar = reinterpret_cast<uint64_t*>(smem + L.ebar);
-    volatile int* ectl = reinterpret_cast<volatile int*>(smem + L.ectl);  // [0] consumer offset, [1] stop
+    float2* ering = reinterpret_cast<float2*>(smem + L.ering);            // ensemble θ bracket ring
+    uint64_t* ebar = reinterpret_cast<uint64_t*>(smem + L.ebar);          // [0, NB) full, [NB, 2NB) empty
+    volatile int* ectl = reinterpret_cast<volatile int*>(smem + L.ectl);  // [1] stop
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.misc + 8);
     const bool lanew = warp < 4;                 // lane warps: thread v owns TMEM lane v (one per v)
     const bool roww = warp < TCS_RW;             // row warps: window rows 2h, 2h + 1 (h = warp / 4)
@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(tcs_nt<ENS>(), ENS ? 2 : 1) k_sa_scratch(const
     if (warp == 0) tc::tmem_alloc(tmem_slot, tcs_cols<ENS>());
     if (t == 0) tc::mbar_init(mbar, 1);
     if (ENS && t == 0) {                         // θ producer ring: block barriers, consumer offset 0, no stop
-        for (int b = 0; b < TCS_ERING / TCS_EB; ++b) tc::mbar_init(reinterpret_cast<uint64_t*>(smem + L.ebar) + b, 1);
+        for (int b = 0; b < 2 * (TCS_ERING / TCS_EB); ++b) tc::mbar_init(reinterpret_cast<uint64_t*>(smem + L.ebar) + b, 1);
         reinterpret_cast<int*>(smem + L.ectl)[0] = 0;
         reinterpret_cast<int*>(smem + L.ectl)[1] = 0;
     }
@@ -206,7 +206,6 @@ __global__ void __launch_bounds__(tcs_nt<ENS>(), ENS ? 2 : 1) k_sa_scratch(const
     const int wmax = a.wmax;
     int W = wmax;
     int parity = 0;
-    int rejI = rej_bound(sch, k0);
     const uint32_t id_gh = tc::idesc_i8(128, 256, true);
     const int kofs0 = RING ? (int)(k0 - TR.kb) : 0;   // ring offset of iteration k0
 #ifdef QAPSA_PHASE_TIMERS
@@ -228,8 +227,7 @@ __global__ void __launch_bounds__(tcs_nt<ENS>(), ENS ? 2 : 1) k_sa_scratch(const
     uint32_t gv[2];
     ScWin wg = sc_win(n, u0, v0, W, kr_end - kr, h2);
     int ring_blo = -1, ring_hi = 0;              // ring: last block refilled from, offsets known resident
-    int ering_ready = 0;                         // ensemble: producer blocks known complete
-    float Tw = 0.0f;
+    int ering_ready = 0, ering_freed = 0;        // ensemble: producer blocks known complete / released
     static_assert(TH_BLK == 1024, "ring_blo counts 1024-iteration blocks");
     while (kr < kr_end && kr - kr_last < gap) {
         // ---------------- window: rows u0 .. u0+R-1 (R <= 4) ----------------
@@ -246,16 +244,17 @@ __global__ void __launch_bounds__(tcs_nt<ENS>(), ENS ? 2 : 1) k_sa_scratch(const
                 ring_hi = (int)(TR.ready * TH_BLK);
             }
         } else {                                 // ensemble: the producer warp's ring
-            if (t == 0) *ectl = (int)kr;         // blocks below kr may be refilled
+            constexpr int NB = TCS_ERING / TCS_EB;
+            if (t == 0) {                        // blocks wholly below kr are consumed: free their slots
+                for (; ering_freed < (int)(kr / TCS_EB); ++ering_freed) tc::mbar_arrive(ebar + NB + (ering_freed % NB));
+            }
             if ((int)kr + Wl > ring_hi) {
                 while (ering_ready * TCS_EB < (int)kr + Wl) {
-                    constexpr int NB = TCS_ERING / TCS_EB;
                     tc::mbar_wait(ebar + (ering_ready % NB), (uint32_t)((ering_ready / NB) & 1));
                     ++ering_ready;
                 }
                 ring_hi = ering_ready * TCS_EB;
             }
-            Tw = temp32(sch, k0 + kr);           // T at the window's first iteration (>= T_k of the window)
         }
         if (fresh) {
             if (mma_pending) {                   // G, H complete before they are read
@@ -301,13 +300,12 @@ __global__ void __launch_bounds__(tcs_nt<ENS>(), ENS ? 2 : 1) k_sa_scratch(const
                 acc_mask |= (unsigned)(ex && (dd[e] <= thr || (thr < 0 && dd[e] <= 0))) << e;   // (R5)
                 need |= (unsigned)(ex && thr < 0 && dd[e] > 0) << e;
             } else {
-                // ensemble: θ_k from the producer's ring (prepare_theta), decided outside its margin
-                // (T = Tw >= T_k), exact double test inside it (R16); δ <= 0 accepted (R5)
-                const float th = ering[((int)kr + o) & (TCS_ERING - 1)];
-                const float m = 2e-4f * th + 2e-5f * Tw;
+                // ensemble: θ_k -+ its margin from the producer's ring (prepare_theta), decided
+                // outside the bracket, exact double test inside it (R16); δ <= 0 accepted (R5)
+                const float2 th = ering[((int)kr + o) & (TCS_ERING - 1)];
                 const float df = (float)dd[e];
-                acc_mask |= (unsigned)(ex && (dd[e] <= 0 || df < th - m)) << e;
-                band |= (unsigned)(ex && dd[e] > 0 && !(df < th - m) && !(df > th + m)) << e;
+                acc_mask |= (unsigned)(ex && (dd[e] <= 0 || df < th.x)) << e;
+                band |= (unsigned)(ex && dd[e] > 0 && !(df < th.x) && !(df > th.y)) << e;
             }
         }
         if (__any_sync(0xffffffffu, (need | band) != 0)) {   // general test: float θ, exact inside its margin
@@ -365,7 +363,6 @@ __global__ void __launch_bounds__(tcs_nt<ENS>(), ENS ? 2 : 1) k_sa_scratch(const
             win_advance<4>(n, u0, v0, Wl, &u0, &v0);
             W = min(2 * W, wmax);
             wg = sc_win(n, u0, v0, W, kr_end - kr, h2);
-            if (!RING) rejI = rej_bound(sch, k0 + kr);   // (the ring path needs no certain-reject bound)
             fresh = true;
             continue;
         }
@@ -472,7 +469,6 @@ __global__ void __launch_bounds__(tcs_nt<ENS>(), ENS ? 2 : 1) k_sa_scratch(const
         ++accepted;
         kr = kracc + 1;
         kr_last = kr;
-        if (!RING) rejI = rej_bound(sch, k0 + kr);
     }
     if (mma_pending) {                           // the last update complete before tensor memory is freed
         tc::mbar_wait(mbar, ph);
@@ -487,17 +483,17 @@ __global__ void __launch_bounds__(tcs_nt<ENS>(), ENS ? 2 : 1) k_sa_scratch(const
     // ---------------- ensemble θ producer: θ_k of the coming iterations, block by block ----------------
     constexpr int NB = TCS_ERING / TCS_EB;
     for (uint32_t b = 0; (uint64_t)b * TCS_EB < (uint64_t)kr_end; ++b) {
-        if (b >= (uint32_t)NB) {                 // the slot's previous block consumed?
-            const int need_off = (int)((b - NB + 1) * TCS_EB);
-            bool stop = false;
-            while (ectl[0] < need_off && !(stop = ectl[1] != 0)) __nanosleep(64);
-            if (stop) break;
+        if (b >= (uint32_t)NB) {                 // the slot's previous block released by the consumers
+            const uint64_t* eb = ebar + NB + (b % NB);
+            const uint32_t par = ((b / NB) - 1) & 1;
+            while (!tc::mbar_try(const_cast<uint64_t*>(eb), par))   // (suspends in hardware between probes)
+                if (ectl[1] != 0) goto produced;
         }
         for (int i = lane; i < TCS_EB; i += 32) {
             Prep pr;
             pr.k = k0 + (uint64_t)b * TCS_EB + (uint64_t)i;
             prepare_theta(pr, sch, seed, cv.chain);
-            ering[(b * TCS_EB + i) & (TCS_ERING - 1)] = pr.th;
+            ering[(b * TCS_EB + i) & (TCS_ERING - 1)] = make_float2(pr.th - pr.m, pr.th + pr.m);
         }
         __syncwarp();
         if (lane == 0) {
@@ -506,6 +502,7 @@ __global__ void __launch_bounds__(tcs_nt<ENS>(), ENS ? 2 : 1) k_sa_scratch(const
         }
         if (ectl[1] != 0) break;
     }
+  produced:;
   } else {
     // ---------------- helper warp: the update MMA of each accept, digest ----------------
     for (uint64_t na = 0;; ++na) {
