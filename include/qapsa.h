@@ -56,7 +56,8 @@ typedef enum {
     QAP_E_NOMEM = 9        /* device or host allocation failed */
 } qap_status;
 
-#define QAP_MAX_N 512   /* and A, B' must fit in one SM's shared memory (else QAP_E_UNSUPPORTED) */
+#define QAP_MAX_N 512   /* and A, B' must fit in one SM's shared memory, or the chain in a cluster's (cluster
+                           engine, 8-bit A); else QAP_E_UNSUPPORTED */
 
 typedef enum { QAP_COOL_GEOMETRIC = 0, QAP_COOL_LUNDY_MEES = 1 } qap_cooling;
 
@@ -236,17 +237,22 @@ typedef enum {
     QAP_OPT_RELABEL_CLUSTER = 8, /* relabel engine: 8 (default) = one chain on a thread-block
                                     cluster of 8 SMs, Δ spread over their shared memory (SURVEY
                                     f1); 1 = one SM, Δ in L2 */
-    QAP_OPT_PROPOSAL = 9         /* candidate order: 0 (default) = the sequential cyclic
+    QAP_OPT_PROPOSAL = 9,        /* candidate order: 0 (default) = the sequential cyclic
                                     enumeration (R4); 1 = random pairs, iteration k proposes pair
                                     index floor(x M / 2^32), x = Philox(seed; k, chain, tag 3)
                                     (R22); runs on the shared-memory kernel (single chain and
                                     qap_ensemble_run) */
+    QAP_OPT_CLUSTER_ENGINE = 10  /* cluster engine (f1; one chain spread over the
+                                    shared memory of a thread-block cluster of 8 SMs, rows of A,
+                                    B' and Δ distributed, N up to QAP_MAX_N): 1 (default) = only
+                                    for chains no single SM holds (N > 256, 8-bit A); 2 = always
+                                    (8-bit A, n >= 4); 0 = never.  Same trajectory either way. */
 } qap_option;
 qap_status qap_set_option(qap_ctx* ctx, int32_t key, int64_t value);
 /* 1 if the next qap_sa_run uses the tensor-memory engine (QAP_OPT_TENSOR_CORE), else 0. */
 int32_t qap_uses_tensor_core(const qap_ctx* ctx);
 /* The engine the next qap_sa_run uses (QAP_ENGINE_*), -1 if ctx is NULL. */
-enum { QAP_ENGINE_SHARED_MEMORY = 0, QAP_ENGINE_TENSOR_MEMORY = 1, QAP_ENGINE_RELABEL = 2 };
+enum { QAP_ENGINE_SHARED_MEMORY = 0, QAP_ENGINE_TENSOR_MEMORY = 1, QAP_ENGINE_RELABEL = 2, QAP_ENGINE_CLUSTER = 3 };
 int32_t qap_engine(const qap_ctx* ctx);
 
 /* Device time in milliseconds of the last qap_sa_run kernel (CUDA events

@@ -20,6 +20,7 @@
 #include "tc_chain.cuh"
 #include "scratch_chain.cuh"
 #include "relabel_chain.cuh"
+#include "cluster_chain.cuh"
 
 using namespace qapsa;
 
@@ -48,6 +49,7 @@ struct qap_ctx {
     bool delta_valid = false;
     bool sticky = false;
     std::string err;
+    int use_cluster = 1;                 // QAP_OPT_CLUSTER_ENGINE: 0 never, 1 when needed (default), 2 always
     int wmax = 0 /* auto */, threads = 0 /* auto */, force_global = 0, ens_group = 128;
     int smem_optin = 0, num_sms = 0;
     bool tc_ok = false;                 // instance fits the tensor-memory engine (tc_chain.cuh)
@@ -217,6 +219,17 @@ static bool use_relabel_engine(const qap_ctx* c) {
            rlb_layout(c->n, c->rlb_cluster).bytes <= c->smem_optin;
 }
 
+// The cluster engine (cluster_chain.cuh, f1) runs the chains that fit no single SM: N > 256, or
+// whatever the other engines cannot hold on chip; QAP_OPT_CLUSTER_ENGINE = 2 forces it (tests).
+static bool cluster_fits(const qap_ctx* c) {
+    return c->ta == 1 && c->proposal == 0 && c->n >= 4 && cl_layout(c->n, c->tb).bytes <= c->smem_optin;
+}
+static bool use_cluster_engine(const qap_ctx* c) {
+    if (!c->use_cluster || !cluster_fits(c)) return false;
+    if (c->use_cluster == 2) return true;
+    return c->n > RLB_MAXN || chain_smem_bytes(c, 256, false) > c->smem_optin;
+}
+
 static qap_status validate_schedule(qap_ctx* c, const qap_schedule* s, uint64_t k0, uint64_t iters,
                                     Sched* out) {
     if (!s) return fail(c, QAP_E_INVALID_ARG, "schedule is NULL");
@@ -337,10 +350,11 @@ qap_status qap_create(int32_t n, const int32_t* A, const int32_t* B, const int32
         delete c;
         return fail(nullptr, QAP_E_CUDA, "cudaSetDevice failed");
     }
-    // A and B' must fit on one SM (Δ may spill to global memory / L2).
-    if (chain_smem_bytes(c, 256, false) > c->smem_optin) {
+    // A and B' must fit on one SM (Δ may spill to global memory / L2), or the chain must fit the
+    // shared memory of a cluster (cluster engine, f1)
+    if (chain_smem_bytes(c, 256, false) > c->smem_optin && !cluster_fits(c)) {
         delete c;
-        return fail(nullptr, QAP_E_UNSUPPORTED, "A and B' do not fit in one SM's shared memory");
+        return fail(nullptr, QAP_E_UNSUPPORTED, "the chain fits neither one SM nor a cluster's shared memory");
     }
     const size_t nA = (size_t)n * c->ld * c->ta, nB = (size_t)n * c->ld * c->tb;
     auto hA = c->ta == 1 ? compact<uint8_t>(n, c->ld, A) : compact<uint16_t>(n, c->ld, A);
@@ -528,12 +542,14 @@ qap_status qap_sa_run(qap_ctx* c, uint64_t k0, uint64_t iters, const qap_schedul
     CU(cudaMemcpyAsync(&before, c->dst, sizeof before, cudaMemcpyDeviceToHost, c->stream));
     CU(cudaMemcpyAsync(&near_before, c->dnear_count, sizeof near_before, cudaMemcpyDeviceToHost, c->stream));
 
-    const bool tc = use_tc_engine(c);
-    const bool rlb = !tc && use_relabel_engine(c);
+    const bool clu = use_cluster_engine(c);
+    const bool tc = !clu && use_tc_engine(c);
+    const bool rlb = !clu && !tc && use_relabel_engine(c);
     const bool explicit_threads = c->threads != 0;
-    const int threads = tc ? TCK_NT : effective_threads(c, explicit_threads ? c->threads : auto_threads(c));
+    const int threads = tc ? TCK_NT : clu ? CLC_NT : effective_threads(c, explicit_threads ? c->threads : auto_threads(c));
     bool ds = !c->force_global && chain_smem_bytes(c, threads, true) <= c->smem_optin;
-    const int smem = tc ? tc_layout(c->ld).bytes
+    const int smem = clu ? cl_layout(c->n, c->tb).bytes
+                   : tc ? tc_layout(c->ld).bytes
                         : rlb ? rlb_layout(c->n, c->rlb_cluster).bytes
                               : chain_smem_bytes(c, threads, ds);
     if (smem > c->smem_optin) return fail(c, QAP_E_UNSUPPORTED, "chain state does not fit on chip");
@@ -550,7 +566,7 @@ qap_status qap_sa_run(qap_ctx* c, uint64_t k0, uint64_t iters, const qap_schedul
 
     a.theta = nullptr; a.theta_hdr = nullptr;
     a.theta_kb = a.theta_cnt = 0;
-    if (tc) {   // θ buffer of one chunk of the call (theta_ring.cuh)
+    if (tc || clu) {   // threshold buffer of one chunk of the call (theta_ring.cuh)
         const size_t need = (size_t)((std::min<uint64_t>(iters, TH_CHUNK) + TH_BLK - 1) / TH_BLK) * TH_BLK;
         if (c->theta_cap < need) {
             if (c->dtheta) cudaFree(c->dtheta);
@@ -618,6 +634,26 @@ qap_status qap_sa_run(qap_ctx* c, uint64_t k0, uint64_t iters, const qap_schedul
                 scratch = kr >= ke;
             }
         }
+    } else if (clu) {
+        // chunks of TH_CHUNK iterations: thresholds of the chunk on the whole GPU, then the cluster
+        auto kern = c->tb == 1 ? k_sa_cluster<uint8_t> : k_sa_cluster<uint16_t>;
+        CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        for (uint64_t kc = k0; kc < k0 + iters; kc += TH_CHUNK) {
+            const uint64_t ke = std::min<uint64_t>(k0 + iters, kc + TH_CHUNK);
+            const uint64_t cnt = (ke - kc + TH_BLK - 1) / TH_BLK * TH_BLK;
+            k_theta<<<c->num_sms * 8, 256, 0, c->stream>>>(sch, seed, 0u, kc, cnt, c->dtheta, c->dtheta_hdr);
+            CU(cudaGetLastError());
+            a.k0 = kc;
+            a.k_end = ke;
+            a.theta = c->dtheta;
+            a.theta_hdr = c->dtheta_hdr;
+            a.theta_kb = kc;
+            a.theta_cnt = cnt;
+            a.k0_dev = nullptr;
+            kern<<<CLC, CLC_NT, smem, c->stream>>>(a);   // one cluster (__cluster_dims__)
+            CU(cudaGetLastError());
+            launches += 2;
+        }
     } else if (rlb) {
         RelabelArgs ra;
         ra.c = a;
@@ -660,7 +696,7 @@ qap_status qap_sa_run(qap_ctx* c, uint64_t k0, uint64_t iters, const qap_schedul
         CU(cudaEventElapsedTime(&c->last_scratch_ms, c->ev0, c->evm));
         CU(cudaMemcpy(c->last_scratch, c->dkout, sizeof c->last_scratch, cudaMemcpyDeviceToHost));
     }
-    c->last_launches = tc ? launches : 1;
+    c->last_launches = (tc || clu) ? launches : 1;
     if (out) {
         out->iterations = iters;
         out->accepted = after.accepted - before.accepted;
@@ -1050,6 +1086,10 @@ qap_status qap_set_option(qap_ctx* c, int32_t key, int64_t value) {
             if (value != 0 && value != 1) return fail(c, QAP_E_INVALID_ARG, "proposal must be 0 or 1");
             c->proposal = (int)value;
             return QAP_OK;
+        case QAP_OPT_CLUSTER_ENGINE:
+            if (value < 0 || value > 2) return fail(c, QAP_E_INVALID_ARG, "cluster engine must be 0, 1 or 2");
+            c->use_cluster = (int)value;
+            return QAP_OK;
         case QAP_OPT_RELABEL_CLUSTER:
             if (value != 1 && value != 8) return fail(c, QAP_E_INVALID_ARG, "relabel cluster must be 1 or 8");
             c->rlb_cluster = (int)value;
@@ -1066,6 +1106,7 @@ int32_t qap_uses_tensor_core(const qap_ctx* c) { return (c && use_tc_engine(c)) 
 
 int32_t qap_engine(const qap_ctx* c) {
     if (!c) return -1;
+    if (use_cluster_engine(c)) return QAP_ENGINE_CLUSTER;
     if (use_tc_engine(c)) return QAP_ENGINE_TENSOR_MEMORY;
     if (use_relabel_engine(c)) return QAP_ENGINE_RELABEL;
     return QAP_ENGINE_SHARED_MEMORY;

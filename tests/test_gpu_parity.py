@@ -479,6 +479,55 @@ def test_config4_full_run_vs_oracle_goldens():
     assert k == cfg["iters"]
 
 
+# ---------------- f1: the cluster engine (cluster_chain.cuh): rows of A, B' and Δ over 8 SMs ----------------
+
+CLU = Q.QAP_OPT_CLUSTER_ENGINE
+
+
+@pytest.mark.parametrize("n,I", [(12, 50000), (50, 100000), (100, 100000), (129, 60000)])
+def test_cluster_engine_forced_small(n, I):
+    """QAP_OPT_CLUSTER_ENGINE = 2 runs the cluster engine on instances other engines also take:
+    bit-exact against the oracle (Δ after the run included), in three calls (resume by k0)."""
+    A, B = taixxa(n, 900 + n)
+    p0 = start_perm(n, 11, 0)
+    sch = O.geometric_schedule_for(A, B, p0, I)
+    with Q.Solver(A, B, p0) as s:
+        s.set_option(CLU, 2)
+        assert s.engine() == Q.QAP_ENGINE_CLUSTER
+    _compare_run(A, B, p0, I, sch, opts=[(CLU, 2)], k_splits=[0, I // 3, I // 2, I])
+
+
+@pytest.mark.parametrize("n", [384, 512])
+def test_cluster_engine_large_n(n):
+    """N beyond one SM (up to QAP_MAX_N = 512) is accepted and runs on the cluster engine: Δ-init
+    against the oracle's, then a 1e5-iteration trajectory bit-exact against the oracle (SCRATCH
+    mode: δ from its definition, Δ compared with a from-scratch rebuild at the end)."""
+    A, B = taixxa(n, 4000 + n)
+    p0 = start_perm(n, 13, 0)
+    I = 100000
+    with Q.Solver(A, B, p0) as s:
+        assert s.engine() == Q.QAP_ENGINE_CLUSTER
+        s.delta_init()
+        _, _, D = s.state()
+        np.testing.assert_array_equal(D.astype(np.int64), O.delta_init(A, O.bprime(B, p0)))
+    sch = O.geometric_schedule_for(A, B, p0, I)
+    g, acc = _compare_run(A, B, p0, I, sch, mode=O.MODE_SCRATCH)
+    assert acc > 1000
+
+
+def test_cluster_engine_uint16_b():
+    """16-bit B on the cluster engine (N = 300 > 256, entries up to 2000)."""
+    n = 300
+    A, _ = taixxa(n, 301)
+    _, B = taixxa(n, 302, 0, 2000)
+    p0 = start_perm(n, 17, 0)
+    I = 60000
+    with Q.Solver(A, B, p0) as s:
+        assert s.engine() == Q.QAP_ENGINE_CLUSTER
+    sch = O.geometric_schedule_for(A, B, p0, I)
+    _compare_run(A, B, p0, I, sch, mode=O.MODE_SCRATCH, k_splits=[0, 25000, I])
+
+
 def test_qaplib_fixture_through_the_abi():
     """f4: a QAPLIB-format instance read from tests/golden goes through qap_create like any
     other; the run is bit-exact against the oracle and reaches the brute-force optimum."""
