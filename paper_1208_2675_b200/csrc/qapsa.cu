@@ -566,7 +566,7 @@ qap_status qap_sa_run(qap_ctx* c, uint64_t k0, uint64_t iters, const qap_schedul
 
     a.theta = nullptr; a.theta_hdr = nullptr;
     a.theta_kb = a.theta_cnt = 0;
-    if (tc || clu) {   // threshold buffer of one chunk of the call (theta_ring.cuh)
+    if (tc || clu || rlb) {   // threshold buffer of one chunk of the call (theta_ring.cuh)
         const size_t need = (size_t)((std::min<uint64_t>(iters, TH_CHUNK) + TH_BLK - 1) / TH_BLK) * TH_BLK;
         if (c->theta_cap < need) {
             if (c->dtheta) cudaFree(c->dtheta);
@@ -666,6 +666,21 @@ qap_status qap_sa_run(qap_ctx* c, uint64_t k0, uint64_t iters, const qap_schedul
         auto kern = CL == 8 ? (c->n == 256 ? k_sa_relabel<256, 8> : k_sa_relabel<0, 8>)
                             : (c->n == 256 ? k_sa_relabel<256, 1> : k_sa_relabel<0, 1>);
         CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        // exact integer thresholds of the call (theta_ring.cuh, R23), then the chain: one launch
+        // per chunk of TH_CHUNK iterations, Δ~ handed over in location space between launches
+        for (uint64_t kc = k0; kc < k0 + iters; kc += TH_CHUNK) {
+        const uint64_t ke = std::min<uint64_t>(k0 + iters, kc + TH_CHUNK);
+        const uint64_t cnt = (ke - kc + TH_BLK - 1) / TH_BLK * TH_BLK;
+        k_theta<<<c->num_sms * 8, 256, 0, c->stream>>>(sch, seed, 0u, kc, cnt, c->dtheta, c->dtheta_hdr);
+        CU(cudaGetLastError());
+        ra.c.k0 = kc;
+        ra.c.k_end = ke;
+        ra.c.theta = c->dtheta;
+        ra.c.theta_hdr = c->dtheta_hdr;
+        ra.c.theta_kb = kc;
+        ra.c.theta_cnt = cnt;
+        ra.c.D = c->dD;
+        ra.d_out = c->dD2;
         cudaLaunchConfig_t lc = {};
         lc.gridDim = dim3(CL, 1, 1);
         lc.blockDim = dim3(RLB_NT, 1, 1);
@@ -680,6 +695,8 @@ qap_status qap_sa_run(qap_ctx* c, uint64_t k0, uint64_t iters, const qap_schedul
         lc.numAttrs = 1;
         CU(cudaLaunchKernelEx(&lc, kern, ra));
         std::swap(c->dD, c->dD2);              // Δ in location space is in the second buffer
+        launches += 2;
+        }
     } else {
         CU(launch_chain(c, a, threads, explicit_threads, ds, smem));
     }
@@ -696,7 +713,7 @@ qap_status qap_sa_run(qap_ctx* c, uint64_t k0, uint64_t iters, const qap_schedul
         CU(cudaEventElapsedTime(&c->last_scratch_ms, c->ev0, c->evm));
         CU(cudaMemcpy(c->last_scratch, c->dkout, sizeof c->last_scratch, cudaMemcpyDeviceToHost));
     }
-    c->last_launches = (tc || clu) ? launches : 1;
+    c->last_launches = (tc || clu || rlb) ? launches : 1;
     if (out) {
         out->iterations = iters;
         out->accepted = after.accepted - before.accepted;

@@ -19,22 +19,22 @@
 // window; every twin before it is accepted, σ is rotated in one parallel step, and each twin
 // thread adds its accept to a private count and digest (R18 is a sum).
 //
-// Per cross accept (slots a < b), 1024 threads:
+// Per cross accept (slots a < b), 1024 threads per CTA:
+//   window  one candidate per thread, decided by one shared-memory load of the exact integer
+//           threshold of its iteration (k_theta, theta_ring.cuh, R23; flagged iterations take the
+//           general float-θ / exact-double test)
 //   stage   dA_x = A_ax - A_bx, dB_x = B~_ax - B~_bx, D''_x = D_x - dA_x dB_x; Z_a = A_a.B~_b,
-//           Z_b = A_b.B~_a (warps 8..15); the 8 columns of the MMA's B operand (threads 512..639)
-//   touch   the four dot products of every v, X_a = B~_v.A_a, X_b, Y_a = A_v.B~_a, Y_b, are two
-//           GEMVs: ONE tensor-core product [Bh | Bl | A] (256 x 768, u8) x W (768 x 8, u8), with
-//           B~ = 256 Bh + Bl split into bytes and W's columns (A_a;0;0), (A_b;0;0), (0;A_a;0),
-//           (0;A_b;0), (0;0;Bl_a), (0;0;Bh_a), (0;0;Bl_b), (0;0;Bh_b): 2 x 24 tcgen05.mma
-//           (kind::i8, M = 128, N = 8, K = 32, s32 in TMEM, exact).  Warps 0..7 read the
-//           result (one TMEM lane per v) and write δ''(a,v), δ''(b,v) (R10b); on a cluster CTAs 0
-//           and 1 compute one 128-row tile each and store every entry into its owner's share
-//   quads   all threads while the MMAs run: Δ~ += 2(dA_u - dA_v)(dB_u - dB_v) for every pair
-//           off rows a, b (R10), one 16-byte quad at a time; Δ~ in global memory / L2
+//           Z_b = A_b.B~_a (warps 8..15)
+//   quads   all threads: Δ~ += 2(dA_u - dA_v)(dB_u - dB_v) for every pair off rows a, b (R10), one
+//           16-byte quad at a time (on a cluster: the CTA's share, in its shared memory)
+//   touch   the four dot products of every v, X_a = B~_v.A_a, X_b, Y_a = A_v.B~_a, Y_b, on the
+//           CUDA cores (dp4a over the byte planes B~ = 256 Bh + Bl and A, one warp per v); on a
+//           cluster each CTA computes N / 8 rows v and stores δ''(a,v), δ''(b,v) (R10b) into the
+//           owner of the entry (distributed shared memory)
 //   next window: B~ rows / columns a, b exchanged, best_p = q∘σ if the cost improved
 //
-// Shared memory (N = 256): the MMA's A operand [Bh | Bl | A] in the K-major canonical layout
-// (tc_common.cuh), 192 KB, is the only copy of A and B~.
+// Shared memory (N = 256): [Bh | Bl | A] in the K-major canonical layout (tc_common.cuh), 192 KB,
+// is the only copy of A and B~.
 //
 // Citation keys: P:n = PAPER.md line n, R# = DESIGN.md readings.
 #pragma once
@@ -43,13 +43,13 @@
 
 #include "kernels.cuh"
 #include "tc_common.cuh"
+#include "theta_ring.cuh"
 
 namespace qapsa {
 
 constexpr int RLB_NT = 1024;
 constexpr int RLB_MAXN = 256;
 constexpr int RLB_MAXCLS = 4;   // twin classes (>= 2 members) the relabel path handles
-constexpr int RLB_EPI = 256;    // threads [0, 256): MMA issue and touching epilogue (after their quads)
 #ifndef RLB_QB_EXP
 constexpr int RLB_QB = 4;       // quad loads in flight per thread
 #else
@@ -60,9 +60,10 @@ constexpr int RLB_SBO = RLB_K / 16 * 128;        // 8-row group stride of the ca
 constexpr int RLB_BL = 256, RLB_AOFF = 512;      // K offsets of the Bl and A parts
 
 struct RlbLayout {
-    int op1, op2, dsh, rowaddr, qdesc, pt, cls, sig, q, bestp, dg, stg, slots, twm, zz, flags, red,
-        bar, bytes;
+    int op1, dsh, rowaddr, qdesc, pt, cls, sig, q, bestp, dg, stg, slots, twm, zz, flags, red,
+        ring, tbar, bytes;
 };
+constexpr int RLB_RS = 8, RLB_RB = 256;          // threshold ring: 8 blocks of 256 (a window is <= 255)
 // quads of Δ~ owned by each CTA of a cluster of CL (quad g belongs to CTA g % CL)
 __host__ __device__ constexpr int rlb_share(int n, int CL) { return (quad_count(n) + CL - 1) / CL; }
 // CL = 1: Δ~ in global memory, all quad descriptors in shared memory; CL > 1: this CTA's share of
@@ -72,7 +73,6 @@ __host__ __device__ constexpr RlbLayout rlb_layout(int n, int CL = 1) {
     const int n4 = (n + 3) & ~3;
     int o = 0;
     L.op1 = o;     o += RLB_MAXN / 8 * RLB_SBO;          // 256 rows x 768 B, canonical K-major
-    L.op2 = o;     o += RLB_SBO;                        // 8 rows x 768 B
     L.dsh = o;     o += CL > 1 ? rlb_share(n, CL) * 16 : 0;
     L.rowaddr = o; o = align16(o + n * 4);
     L.qdesc = o;   o = align16(o + (CL > 1 ? rlb_share(n, CL) : quad_count(n)) * 2);
@@ -88,7 +88,8 @@ __host__ __device__ constexpr RlbLayout rlb_layout(int n, int CL = 1) {
     L.zz = o;      o = align16(o + 16 * 4);
     L.flags = o;   o = align16(o + 4 * 4);
     L.red = o;     o = align16(o + 2 * 8);
-    L.bar = o;     o = align16(o + 16);                 // mbarrier + TMEM base address
+    L.ring = o;    o += RLB_RS * RLB_RB * 4;            // exact integer thresholds (theta_ring.cuh, R23)
+    L.tbar = o;    o += RLB_RS * 8;
     L.bytes = o;
     return L;
 }
@@ -107,16 +108,6 @@ __device__ __forceinline__ int rlb_off(int x, int k) { return tc::kmaj_off(x, k,
 __device__ __forceinline__ int rlb_A(const uint8_t* op1, int x, int k) { return op1[rlb_off(x, RLB_AOFF + k)]; }
 __device__ __forceinline__ int rlb_B(const uint8_t* op1, int x, int k) {
     return ((int)op1[rlb_off(x, k)] << 8) | (int)op1[rlb_off(x, RLB_BL + k)];
-}
-
-// D[tmem] (+)= A[smem] x B[smem]^T with a compile-time accumulate flag (straight-line issue)
-template <bool ACC>
-__device__ __forceinline__ void rlb_mma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
-        "l"(a), "l"(b), "r"(idesc), "n"(ACC ? 1 : 0)
-        : "memory");
 }
 
 // ---- thread-block cluster helpers (f1: Δ~ spread over the shared memory of CL CTAs)
@@ -159,7 +150,6 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
     const int nql = CL > 1 ? (nqt - crank + CL - 1) / CL : nqt;   // quads this CTA owns
     int32_t* Ds = reinterpret_cast<int32_t*>(smem + L.dsh);       // CL > 1: local share of Δ~
     uint8_t* op1 = smem + L.op1;
-    uint8_t* op2 = smem + L.op2;
     int32_t* rowaddr = reinterpret_cast<int32_t*>(smem + L.rowaddr);
     uint16_t* qdesc = reinterpret_cast<uint16_t*>(smem + L.qdesc);
     uint16_t* pt = reinterpret_cast<uint16_t*>(smem + L.pt);
@@ -174,8 +164,6 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
     int* zz = reinterpret_cast<int*>(smem + L.zz);
     int* flags = reinterpret_cast<int*>(smem + L.flags);
     unsigned long long* red = reinterpret_cast<unsigned long long*>(smem + L.red);
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + L.bar);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.bar + 8);
     int32_t* D = a.D;
     const uint8_t* Ag = reinterpret_cast<const uint8_t*>(a.A);
     const uint16_t* Bg = reinterpret_cast<const uint16_t*>(a.B);   // 16-bit B (ra.b8 == 0)
@@ -194,15 +182,13 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
     if (CL > 1)
         for (int i = t; i < nql; i += RLB_NT)
             reinterpret_cast<int4*>(Ds)[i] = reinterpret_cast<const int4*>(a.D)[crank + CL * i];
-    for (int i = t; i < RLB_SBO / 16; i += RLB_NT) reinterpret_cast<uint4*>(op2)[i] = make_uint4(0, 0, 0, 0);
     if (t < 4) flags[t] = 0;
     if (t < 2) red[t] = 0ull;
-    if (t == 0) tc::mbar_init(mbar, 1);
-    if (warp == 0) tc::tmem_alloc(tmem_slot, 32);
-    tc::fence_before_sync();
+    ThetaRing<RLB_RS, RLB_RB> TR = theta_ring<RLB_RS, RLB_RB>(
+        reinterpret_cast<int*>(smem + L.ring), nullptr, reinterpret_cast<uint64_t*>(smem + L.tbar), a.theta,
+        nullptr, a.theta_kb, a.theta_cnt, a.k0);
+    if (t == 0 && a.k0 < a.k_end) TR.start(a.k0);
     __syncthreads();
-    tc::fence_after_sync();
-    const uint32_t tmem = *tmem_slot;
     // op1 = [Bh | Bl | A] of the slots: B~ = B[q][q] split into bytes, A (zero beyond n)
     for (int idx = t; idx < RLB_MAXN * (RLB_K / 4); idx += RLB_NT) {
         const int x = idx / (RLB_K / 4), k = 4 * (idx - x * (RLB_K / 4));
@@ -225,7 +211,6 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
         }
         *reinterpret_cast<uint32_t*>(op1 + rlb_off(x, k)) = w;
     }
-    tc::fence_proxy_async();                              // op1 / op2 -> tensor-core operand reads
     __syncthreads();
     for (int x = t; x < n; x += RLB_NT) {
         int acc = 0;
@@ -263,9 +248,10 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
     int r, s0;
     tri_pair(n, (int)(k % (uint64_t)M), &r, &s0);
     int parity = 0, pa = -1, pb = -1;
-    uint32_t mma_phase = 0;
     float rejT = 38.5f * temp32(a.sch, k);
-    const uint32_t idesc = tc::idesc_i8(128, 8, false);   // u8 x u8 -> s32, M = 128, N = 8
+    int ring_blo = -1, ring_hi = 0;
+    // touching rows of this CTA: [vlo, vhi) (a cluster splits the N rows into CL slices)
+    const int vrows = (n + CL - 1) / CL, vlo = crank * vrows, vhi = min(n, vlo + vrows);
 
     while (k < k_end) {
         const uint64_t remaining = k_end - k;
@@ -297,12 +283,22 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
                     *Sw = (x & ~m) | (y & m);             // their values (B~ symmetric, zero diag)
                 }
             }
-            tc::fence_proxy_async();                      // op1 writes -> next MMA's operand reads
             if (flags[0])
                 for (int x = t; x < n; x += RLB_NT) bestp[x] = q[sig[x]];
             pa = -1;
         }
 
+        {   // thresholds of the window's iterations resident (theta_ring.cuh)
+            const int ko = (int)(k - TR.kb);
+            if (t == 0 && (ko >> 8) != ring_blo) {
+                ring_blo = ko >> 8;
+                TR.refill(k);
+            }
+            if (ko + Wl > ring_hi) {
+                TR.ensure_ofs(ko + Wl);
+                ring_hi = (int)(TR.ready * RLB_RB);
+            }
+        }
         if (CL > 1 && pend_wait) { cl_wait(); pend_wait = false; }   // other CTAs' updates visible
         // ---- window: candidates (r, s0 + t), t < Wl
         const int cr = ncls ? cls[r] : 0xFF;
@@ -320,9 +316,12 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
                 const int sa = min(sr, ss), sb = max(sr, ss);
                 sab = (sa << 16) | sb;
                 d = drd(rowaddr[sa] + sb);
-                if (d <= 0) {
-                    acc = true;                           // δ < 0, or δ = 0: exp(0) = 1 > r (R5)
-                } else if ((float)d <= rejT) {            // else certain reject (chain.cuh)
+                // exact integer threshold (R23); δ <= 0 accepted (R5); a flagged iteration takes
+                // the general test (float θ with a margin, exact inside it, near ties flagged)
+                const int thr = TR.at_ofs((int)(k - TR.kb) + t);
+                if (d <= thr || d <= 0) {
+                    acc = true;
+                } else if (thr < 0 && (float)d <= rejT) {  // else certain reject (chain.cuh)
                     acc = metropolis_fast(d, a.sch, k + (uint64_t)t, a.seed, 0u, &near);
                 }
             }
@@ -367,7 +366,7 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
         }
 
         // ---- cross accept: slots (sa, sb), location pair (r, sl)
-        if (CL > 1) cl_arrive();                          // this CTA's window reads are done
+        if (CL > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");   // window reads done (nothing to publish)
         const int4 win = slots[j >> 5];
         const int dw = win.y, sa = win.z >> 16, sb = win.z & 0xFFFF, sl = win.w;
         const uint64_t kacc = k + (uint64_t)j;
@@ -391,43 +390,11 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
             zb = __reduce_add_sync(0xffffffffu, zb);
             if (lane == 0) { zz[2 * (warp - 8)] = za; zz[2 * (warp - 8) + 1] = zb; }
         }
-        if (t >= 512 && t < 640) {                        // W: 8 columns x 16 chunks of 16 bytes
-            const int col = (t - 512) >> 4, c16 = 16 * ((t - 512) & 15);
-            const int row = (col & 1) ? sb : sa;
-            int ksrc, kdst;
-            if (col < 4) { ksrc = RLB_AOFF + c16; kdst = (col < 2 ? 0 : RLB_BL) + c16; }
-            else { ksrc = (col == 4 || col == 6) ? RLB_BL + c16 : c16; kdst = RLB_AOFF + c16; }
-            const int rowx = col < 4 ? row : ((col < 6) ? sa : sb);
-            *reinterpret_cast<uint4*>(op2 + rlb_off(col, kdst)) =
-                *reinterpret_cast<const uint4*>(op1 + rlb_off(rowx, ksrc));
-            tc::fence_proxy_async();
-        }
         __syncthreads();
         const int ars = rlb_A(op1, sa, sb), brs = rlb_B(op1, sa, sb);
         int Da = ars * brs, Db = ars * brs;               // D''_a = A_a.B~_b + a_ab B~_ab, D''_b
 #pragma unroll
         for (int w = 0; w < 8; ++w) { Da += zz[2 * w]; Db += zz[2 * w + 1]; }
-        // tiles of the touching product this CTA computes: both on one SM; on a cluster, CTA c
-        // computes rows [128c, 128c + 128) (c < 2) and stores each touching entry to its owner
-        const int ntile = (n + 127) / 128;
-        const bool mine = CL == 1 || crank < ntile;
-        // touching dot products on the tensor cores (issued now, read after the quads)
-        if (t == 0 && mine) {
-            // descriptors advance by 256 bytes (one K = 32 step) = 16 in the address field
-            tc::fence_after_sync();
-            const uint64_t bd = tc::smem_desc(tc::smem_u32(op2), 128, RLB_SBO);
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                if (c == 1 && n <= 128) break;
-                if (CL > 1 && c != crank) continue;
-                const uint64_t ad = tc::smem_desc(tc::smem_u32(op1) + c * 16 * RLB_SBO, 128, RLB_SBO);
-                rlb_mma<false>(tmem + 8 * c, ad, bd, idesc);
-#pragma unroll
-                for (int kk = 1; kk < RLB_K / 32; ++kk)
-                    rlb_mma<true>(tmem + 8 * c, ad + 16 * kk, bd + 16 * kk, idesc);
-            }
-            tc::mma_commit(mbar);
-        }
         if (t == RLB_NT - 1) {                            // scalar state (row sa is off the quads)
             const uint16_t x = q[sa];
             q[sa] = q[sb];
@@ -516,36 +483,60 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
                 }
             }
         }
-        // touching entries: warps 0..7, one TMEM lane (= one v) per thread
+        // touching entries (R10b) of this CTA's rows v in [vlo, vhi) on the CUDA cores: the four
+        // dot products X_a = B~_v.A_a, X_b, Y_a = A_v.B~_a, Y_b by dp4a over the byte planes
+        // B~ = 256 Bh + Bl and A.  A warp takes 8 rows v = v8 .. v8 + 7 (one 8-row group of the
+        // canonical layout, so the 8 lanes of a quarter warp read 128 contiguous bytes): lane l
+        // handles row v8 + (l & 7) and the 16-byte K chunks l / 8, + 4, + 8, + 12; the 4 partial
+        // sums of a row are added with two shuffles.  Lane l (l < 8) keeps row v8 + l's entries.
         int wa = -1, wb = -1, va = 0, vb = 0;
-        if (t < RLB_EPI && mine) {
-            const int c = CL > 1 ? crank : warp >> 2;
-            const bool act = CL > 1 ? warp < 4 : 128 * c < n;
-            const int v = 128 * c + 32 * (warp & 3) + lane;
-            if (act) {
-                tc::mbar_wait(mbar, mma_phase);
-                tc::fence_after_sync();
-                uint32_t R[8];
-                tc::tmem_ld8(tmem + ((uint32_t)(32 * (warp & 3)) << 16) + 8 * c, R);
-                tc::tmem_wait_ld();
-                if (v < n && v != sa && v != sb) {
-                    const int xa = ((int)R[0] << 8) + (int)R[2];  // X_a = B~_v.A_a
-                    const int xb = ((int)R[1] << 8) + (int)R[3];  // X_b = B~_v.A_b
-                    const int ya = (int)R[4] + ((int)R[5] << 8);  // Y_a = A_v.B~_a
-                    const int yb = (int)R[6] + ((int)R[7] << 8);  // Y_b = A_v.B~_b
+        {
+            const int rl = lane & 7, cq = lane >> 3;
+            for (int v8 = (vlo & ~7) + 8 * warp; v8 < vhi; v8 += RLB_NT / 4) {
+                const int v = v8 + rl;
+                unsigned s8[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};   // Xa h/l, Xb h/l, Ya h/l, Yb h/l
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int kc = 16 * (cq + 4 * i);
+                    const uint4 Av = *reinterpret_cast<const uint4*>(op1 + rlb_off(v, RLB_AOFF + kc));
+                    const uint4 Hv = *reinterpret_cast<const uint4*>(op1 + rlb_off(v, kc));
+                    const uint4 Lv = *reinterpret_cast<const uint4*>(op1 + rlb_off(v, RLB_BL + kc));
+                    const uint4 Aa = *reinterpret_cast<const uint4*>(op1 + rlb_off(sa, RLB_AOFF + kc));
+                    const uint4 Ab = *reinterpret_cast<const uint4*>(op1 + rlb_off(sb, RLB_AOFF + kc));
+                    const uint4 Ha = *reinterpret_cast<const uint4*>(op1 + rlb_off(sa, kc));
+                    const uint4 La = *reinterpret_cast<const uint4*>(op1 + rlb_off(sa, RLB_BL + kc));
+                    const uint4 Hb = *reinterpret_cast<const uint4*>(op1 + rlb_off(sb, kc));
+                    const uint4 Lb = *reinterpret_cast<const uint4*>(op1 + rlb_off(sb, RLB_BL + kc));
+                    auto dot = [](uint4 x, uint4 y, unsigned c) {
+                        return __dp4a(x.x, y.x, __dp4a(x.y, y.y, __dp4a(x.z, y.z, __dp4a(x.w, y.w, c))));
+                    };
+                    s8[0] = dot(Hv, Aa, s8[0]); s8[1] = dot(Lv, Aa, s8[1]);
+                    s8[2] = dot(Hv, Ab, s8[2]); s8[3] = dot(Lv, Ab, s8[3]);
+                    s8[4] = dot(Av, Ha, s8[4]); s8[5] = dot(Av, La, s8[5]);
+                    s8[6] = dot(Av, Hb, s8[6]); s8[7] = dot(Av, Lb, s8[7]);
+                }
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    s8[e] += __shfl_xor_sync(0xffffffffu, s8[e], 8);
+                    s8[e] += __shfl_xor_sync(0xffffffffu, s8[e], 16);
+                }
+                if (cq == 0 && v >= vlo && v < vhi && v != sa && v != sb) {
+                    const int xa = (int)(s8[0] * 256u + s8[1]);    // X_a = B~_v.A_a
+                    const int xb = (int)(s8[2] * 256u + s8[3]);    // X_b = B~_v.A_b
+                    const int ya = (int)(s8[4] * 256u + s8[5]);    // Y_a = A_v.B~_a
+                    const int yb = (int)(s8[6] * 256u + s8[7]);    // Y_b = A_v.B~_b
                     const int av = rlb_A(op1, sa, v), bv = rlb_A(op1, sb, v);
                     const int abv = rlb_B(op1, sa, v), bbv = rlb_B(op1, sb, v);
                     const int da = av - bv, db = abv - bbv;
                     const int dv = Dg[v];                 // D''_v (updated in the stage)
                     // R10b: δ''(a,v) and δ''(b,v) from pre-swap rows
-                    wa = v > sa ? rowaddr[sa] + v : rowaddr[v] + sa;
-                    va = 2 * (xa + ars * db + yb - da * brs - Da - dv + 2 * av * bbv);
-                    wb = v > sb ? rowaddr[sb] + v : rowaddr[v] + sb;
-                    vb = 2 * (xb - ars * db + ya + da * brs - Db - dv + 2 * bv * abv);
+                    const int ea = v > sa ? rowaddr[sa] + v : rowaddr[v] + sa;
+                    const int fa = 2 * (xa + ars * db + yb - da * brs - Da - dv + 2 * av * bbv);
+                    const int eb = v > sb ? rowaddr[sb] + v : rowaddr[v] + sb;
+                    const int fb = 2 * (xb - ars * db + ya + da * brs - Db - dv + 2 * bv * abv);
+                    wa = ea; va = fa; wb = eb; vb = fb;   // (one pass per warp: rows <= 32 x 8)
                 }
-                tc::fence_before_sync();
             }
-            mma_phase ^= 1;
         }
         __syncthreads();                                  // quads written: columns sa, sb next
         if (wa >= 0) {                                    // this CTA computed them: store anywhere
@@ -583,10 +574,8 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
         atomicAdd(&red[0], my_dig);
         atomicAdd(&red[1], my_cnt);
     }
-    tc::fence_before_sync();
+    if (t == 0) TR.drain();
     __syncthreads();
-    tc::fence_after_sync();
-    if (warp == 0) tc::tmem_dealloc(tmem, 32);
     if (crank == 0)
         for (int x = t; x < n; x += RLB_NT) {
             a.p[x] = q[sig[x]];

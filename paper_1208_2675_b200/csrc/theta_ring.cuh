@@ -113,17 +113,20 @@ __device__ __forceinline__ void fence_mbar_init() {
 }
 }  // namespace tc
 
-// One chain's view of a ring of SLOTS blocks.  Every consumer thread keeps `ready` (blocks known
+// One chain's view of a ring of SLOTS blocks of BS thresholds (BS divides TH_BLK; the block
+// headers are copied only when BS == TH_BLK).  Every consumer thread keeps `ready` (blocks known
 // complete, identical in all threads: they wait in the same order); the issuing thread also keeps
-// `issued`.  A window of w iterations leaves SLOTS - ceil(w / TH_BLK) - 1 blocks of prefetch.
-template <int SLOTS>
+// `issued`.  A window of w iterations leaves SLOTS - ceil(w / BS) - 1 blocks of prefetch.
+template <int SLOTS, int BS = TH_BLK>
 struct ThetaRing {
-    static constexpr int RING = SLOTS * TH_BLK;
+    static_assert(TH_BLK % BS == 0 && BS % 4 == 0, "ring blocks split k_theta's blocks");
+    static constexpr int RING = SLOTS * BS;
+    static constexpr bool HDR = BS == TH_BLK;
     int* ring;                   // shared memory, RING thresholds
-    int4* hring;                 // shared memory, SLOTS block headers
+    int4* hring;                 // shared memory, SLOTS block headers (HDR)
     uint64_t* bars;              // shared memory, SLOTS mbarriers
-    const int* src;              // thresholds of iterations [kb, kb + nblk TH_BLK)
-    const int4* hsrc;            // their block headers
+    const int* src;              // thresholds of iterations [kb, kb + nblk BS)
+    const int4* hsrc;            // their block headers (HDR)
     unsigned long long kb;
     long long nblk;
     long long ready;
@@ -133,13 +136,13 @@ struct ThetaRing {
     // b - SLOTS < b_lo, whose iterations every consumer has passed (a CTA / group barrier
     // separates the last window that read it from this call)
     __device__ __forceinline__ void refill(unsigned long long k) {
-        const long long b_lo = (long long)((k - kb) / TH_BLK);
+        const long long b_lo = (long long)((k - kb) / BS);
         const long long hi = min(nblk, b_lo + SLOTS);
         for (; issued < hi; ++issued) {
             const int slot = (int)(issued & (SLOTS - 1));
-            tc::mbar_expect_tx(bars + slot, TH_BLK * 4 + 16);
-            tc::bulk_g2s(ring + slot * TH_BLK, src + issued * TH_BLK, TH_BLK * 4, bars + slot);
-            tc::bulk_g2s(hring + slot, hsrc + issued, 16, bars + slot);
+            tc::mbar_expect_tx(bars + slot, BS * 4 + (HDR ? 16 : 0));
+            tc::bulk_g2s(ring + slot * BS, src + issued * BS, BS * 4, bars + slot);
+            if (HDR) tc::bulk_g2s(hring + slot, hsrc + issued, 16, bars + slot);
         }
     }
     // thread 0 of the chain before the kernel's first use: barriers, first SLOTS blocks
@@ -154,7 +157,7 @@ struct ThetaRing {
     // every consumer: thresholds of iterations < k_hi resident (block b completes phase
     // (b / SLOTS) & 1)
     __device__ __forceinline__ void ensure(unsigned long long k_hi) {
-        const long long bh = (long long)((k_hi - 1 - kb) / TH_BLK);
+        const long long bh = (long long)((k_hi - 1 - kb) / BS);
         while (ready <= bh) {
             tc::mbar_wait(bars + (int)(ready & (SLOTS - 1)), (uint32_t)((ready / SLOTS) & 1));
             ++ready;
@@ -162,7 +165,7 @@ struct ThetaRing {
     }
     // the same with 32-bit offsets from kb (a launch's range is far below 2^31)
     __device__ __forceinline__ void ensure_ofs(int ofs_hi) {
-        while (ready * TH_BLK < (long long)ofs_hi) {
+        while (ready * BS < (long long)ofs_hi) {
             tc::mbar_wait(bars + (int)(ready & (SLOTS - 1)), (uint32_t)((ready / SLOTS) & 1));
             ++ready;
         }
@@ -171,10 +174,10 @@ struct ThetaRing {
     __device__ __forceinline__ int at(unsigned long long kk) const {
         return ring[(int)((kk - kb) & (unsigned long long)(RING - 1))];
     }
-    // iterations [k_lo, k_hi) (resident): {any flagged, max thr}
+    // iterations [k_lo, k_hi) (resident; HDR): {any flagged, max thr}
     __device__ __forceinline__ int2 span(unsigned long long k_lo, unsigned long long k_hi) const {
         int fl = 0, mx = INT_MIN;
-        for (long long b = (long long)((k_lo - kb) / TH_BLK); b <= (long long)((k_hi - 1 - kb) / TH_BLK); ++b) {
+        for (long long b = (long long)((k_lo - kb) / BS); b <= (long long)((k_hi - 1 - kb) / BS); ++b) {
             const int4 h = hring[(int)(b & (SLOTS - 1))];
             fl |= h.x;
             mx = max(mx, h.y);
@@ -188,21 +191,21 @@ struct ThetaRing {
     }
 };
 
-template <int SLOTS>
-__device__ __forceinline__ ThetaRing<SLOTS> theta_ring(int* ring, int4* hring, uint64_t* bars, const int* src,
-                                                       const int4* hsrc, unsigned long long kb,
-                                                       unsigned long long cnt, unsigned long long k) {
+template <int SLOTS, int BS = TH_BLK>
+__device__ __forceinline__ ThetaRing<SLOTS, BS> theta_ring(int* ring, int4* hring, uint64_t* bars, const int* src,
+                                                           const int4* hsrc, unsigned long long kb,
+                                                           unsigned long long cnt, unsigned long long k) {
     // blocks are counted from the one holding k (a kernel chained after the scratch phase starts
     // inside the buffer): every slot's first use is then phase 0 of its mbarrier
-    const unsigned long long b0 = (k - kb) / TH_BLK;
-    ThetaRing<SLOTS> R;
+    const unsigned long long b0 = (k - kb) / BS;
+    ThetaRing<SLOTS, BS> R;
     R.ring = ring;
     R.hring = hring;
     R.bars = bars;
-    R.src = src + b0 * TH_BLK;
-    R.hsrc = hsrc + b0;
-    R.kb = kb + b0 * TH_BLK;
-    R.nblk = (long long)((cnt + TH_BLK - 1) / TH_BLK) - (long long)b0;
+    R.src = src + b0 * BS;
+    R.hsrc = hsrc + b0 * BS / TH_BLK;
+    R.kb = kb + b0 * BS;
+    R.nblk = (long long)((cnt + BS - 1) / BS) - (long long)b0;
     R.ready = 0;
     R.issued = 0;
     return R;
