@@ -384,6 +384,22 @@ __global__ void __launch_bounds__(tcs_nt<ENS>(), ENS ? 2 : 1) k_sa_scratch(const
             npu[e] = nu[e] == r ? ps : nu[e] == s ? pr : pn;
         }
         TCT_ACC(6, pt1, npu[0] + npu[1]);
+        // shared-memory operands first (independent of the update MMA still in flight)
+        // (v >= n reads padding or the next row: in bounds, and those lanes' values are never used)
+        const int arv = As[r * ld + v], asv = As[s * ld + v];
+        const int bfr = Bs[pr * ld + v], bfs = Bs[ps * ld + v];
+        int dAu[2], dBfu[2];                     // dA of the next rows (locations), dBf of their facilities
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            dAu[e] = (int)As[nu[e] * ld + r] - (int)As[nu[e] * ld + s];
+            dBfu[e] = (int)Bs[npu[e] * ld + pr] - (int)Bs[npu[e] * ld + ps];
+        }
+        int dB = 0, ars = 0, brs = 0;
+        if (h2 == 0) {                           // D'' below (one thread per v)
+            dB = vin ? (int)Bs[pr * ld + px] - (int)Bs[ps * ld + px] : 0;
+            ars = As[r * ld + s];
+            brs = Bs[pr * ld + ps];
+        }
         if (mma_pending) {                       // the previous update complete: tensor memory is current
             if (!mma_done) tc::mbar_wait(mbar, ph);
             ph ^= 1;
@@ -391,26 +407,20 @@ __global__ void __launch_bounds__(tcs_nt<ENS>(), ENS ? 2 : 1) k_sa_scratch(const
         }
         TCT_ACC(7, pt1, ph);
         uint32_t gps = 0, gpr = 0, g4[2], h4[2];   // PRE-update tensor memory
-        if (h2 == 0) {
-            tc::tmem_ld1(tm + quad_lane + TCS_COL_G + (uint32_t)ps, gps);   // G[v][p(s)]
-            tc::tmem_ld1(tm + quad_lane + TCS_COL_G + (uint32_t)pr, gpr);   // G[v][p(r)]
-        }
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
             tc::tmem_ld1(tm + quad_lane + TCS_COL_G + (uint32_t)npu[e], g4[e]);
             tc::tmem_ld1(tm + quad_lane + TCS_COL_H + (uint32_t)nu[e], h4[e]);
         }
-        // (v >= n reads padding or the next row: in bounds, and those lanes' values are never used)
-        const int arv = As[r * ld + v], asv = As[s * ld + v];
-        const int bfr = Bs[pr * ld + v], bfs = Bs[ps * ld + v];
-        const int dA = vin ? arv - asv : 0, dBf = vin ? bfr - bfs : 0;
-        int dAu[2], dBfu[2];                     // dA of the next rows (locations), dBf of their facilities
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-            dAu[e] = (int)As[nu[e] * ld + r] - (int)As[nu[e] * ld + s];
-            dBfu[e] = (int)Bs[npu[e] * ld + pr] - (int)Bs[npu[e] * ld + ps];
+        // G[v][p(s)], G[v][p(r)]: needed by lanes r and s only (their new diagonal), so only the
+        // h2 = 0 warps of those lanes' quadrants load them (warp-uniform)
+        const int q4 = warp & 3;
+        if (h2 == 0 && ((r >> 5) == q4 || (s >> 5) == q4)) {
+            tc::tmem_ld1(tm + quad_lane + TCS_COL_G + (uint32_t)ps, gps);
+            tc::tmem_ld1(tm + quad_lane + TCS_COL_G + (uint32_t)pr, gpr);
         }
-        if (h2 == 0) {                           // the update's operands (one thread per v)
+        const int dA = vin ? arv - asv : 0, dBf = vin ? bfr - bfs : 0;
+        if (h2 != 0) {                           // the update's operands (one thread per v, the h2 = 1 warps)
             const int ro = (v >> 3) * 256 + (v & 7) * 16;
             if (ENS) *reinterpret_cast<uint16_t*>(La + ro) = (uint16_t)(b8(dA) | (b8(-dBf) << 8));   // A row v
             else tc::tmem_st1(tm + quad_lane + TCS_COL_L, b8(dA) | (b8(-dBf) << 8));
@@ -426,16 +436,12 @@ __global__ void __launch_bounds__(tcs_nt<ENS>(), ENS ? 2 : 1) k_sa_scratch(const
             rc[2] = (int)(uint32_t)kacc; rc[3] = (int)(uint32_t)(kacc >> 32);
         }
         TCT_ACC(9, pt1, dAu[1] + dBfu[1] + arv + bfs);
+        tc::tmem_wait_ld();
         if (h2 == 0) {                           // D'' (one thread per v)
-            const int dB = vin ? (int)Bs[pr * ld + px] - (int)Bs[ps * ld + px] : 0;
-            const int ars = As[r * ld + s], brs = Bs[pr * ld + ps];
-            tc::tmem_wait_ld();
             const int dnew = (v == r) ? (int)gps + ars * brs : (v == s) ? (int)gpr + ars * brs : dv - dA * dB;
             if (vin) Dg[v] = dnew;
             if (v == r) p[v] = (uint16_t)ps;
             if (v == s) p[v] = (uint16_t)pr;
-        } else {
-            tc::tmem_wait_ld();
         }
         TCT_ACC(8, pt1, (int)(h4[1] + g4[1]));
         px = (v == r) ? ps : (v == s) ? pr : px;     // p(v), p^-1(v) after the swap
@@ -448,7 +454,7 @@ __global__ void __launch_bounds__(tcs_nt<ENS>(), ENS ? 2 : 1) k_sa_scratch(const
             if (vin) xch[(h2 + e) * 128 + qv] = (int)h4[e] - dBf * dAu[e];  // H''[v][u_i] = G''_{u_i, p''^-1(v)}
         }
         TCT_ACC(2, pt1, gv[1]);
-        if (h2 == 0) {                           // the update's operands visible to the tensor cores
+        if (h2 != 0) {                           // the update's operands visible to the tensor cores
             if (!ENS) tc::tmem_wait_st();
             tc::fence_proxy_async();
         }
