@@ -344,20 +344,13 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
             const int ulo = v >= v0 ? u0 : u0 + 1;
             const int uhi = vin ? min(v - 1, u0 + R - 1) : -1;
             const int kofs = (int)(k - TR.kb);
-            // the next group's cells are loaded while this group is tested (software pipeline:
-            // one tcgen05.ld in flight; waited for before its registers are read or the loop ends)
-            uint32_t dd[8], nx[8];
-            int g = warp >> 2;
-            if (g < NG) {
-                tc::tmem_ld8(tm + quad_lane + (uint32_t)(u0 + 8 * g), dd);
-                tc::tmem_wait_ld();
-            }
-            for (; g < NG; g += 2) {
+            for (int g = warp >> 2; g < NG; g += 2) {
                 const int i0 = 8 * g;
-                const bool more = g + 2 < NG;
-                if (more) tc::tmem_ld8(tm + quad_lane + (uint32_t)(u0 + i0 + 16), nx);
                 int f = i0 == 0 ? 0 : win_f(i0, L0, m1);   // offset of row u0 + i0's first candidate
+                uint32_t dd[8];
+                tc::tmem_ld8(tm + quad_lane + (uint32_t)(u0 + i0), dd);
                 const int lo = ulo - u0 - i0, hi = uhi - u0 - i0;   // this thread's rows i in [lo, hi]
+                tc::tmem_wait_ld();
                 if (v == pend_r || v == pend_s) {    // cells still being patched: their new values
                     const int* row = v == pend_r ? rowR : rowS;
 #pragma unroll
@@ -380,7 +373,6 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
                         am |= (unsigned)(i >= lo && i <= hi && (int)dd[i] <= thr) << i;
                     }
                 }
-                if (more) tc::tmem_wait_ld();    // the next group's cells (also before leaving)
                 if (__any_sync(0xffffffffu, am != 0)) {
                     if (am) {                    // this thread's first accepted candidate
                         const int i = __ffs(am) - 1;
@@ -391,8 +383,6 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
                     }
                     break;
                 }
-#pragma unroll
-                for (int i = 0; i < 8; ++i) dd[i] = nx[i];
             }
         } else
         for (int g = warp >> 2; g < NG; g += 2) {
