@@ -242,11 +242,15 @@ typedef enum {
                                     index floor(x M / 2^32), x = Philox(seed; k, chain, tag 3)
                                     (R22); runs on the shared-memory kernel (single chain and
                                     qap_ensemble_run) */
-    QAP_OPT_CLUSTER_ENGINE = 10  /* cluster engine (f1; one chain spread over the
+    QAP_OPT_CLUSTER_ENGINE = 10, /* cluster engine (f1; one chain spread over the
                                     shared memory of a thread-block cluster of 8 SMs, rows of A,
                                     B' and Δ distributed, N up to QAP_MAX_N): 1 (default) = only
                                     for chains no single SM holds (N > 256, 8-bit A); 2 = always
                                     (8-bit A, n >= 4); 0 = never.  Same trajectory either way. */
+    QAP_OPT_ENSEMBLE_SCRATCH4 = 11 /* tensor-memory ensembles: 1 (default) = the scratch phase of four
+                                    chains per SM (G only in tensor memory, 128 columns; the window's
+                                    rows of G exchanged through shared memory); 0 = two chains per
+                                    SM (G and H).  Same results either way. */
 } qap_option;
 qap_status qap_set_option(qap_ctx* ctx, int32_t key, int64_t value);
 /* 1 if the next qap_sa_run uses the tensor-memory engine (QAP_OPT_TENSOR_CORE), else 0. */

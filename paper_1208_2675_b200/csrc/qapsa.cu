@@ -21,6 +21,7 @@
 #include "scratch_chain.cuh"
 #include "relabel_chain.cuh"
 #include "cluster_chain.cuh"
+#include "ens_chain.cuh"
 
 using namespace qapsa;
 
@@ -49,6 +50,7 @@ struct qap_ctx {
     bool delta_valid = false;
     bool sticky = false;
     std::string err;
+    int ens4 = 1;                        // QAP_OPT_ENSEMBLE_SCRATCH4: ensemble scratch phase 4 chains per SM
     int use_cluster = 1;                 // QAP_OPT_CLUSTER_ENGINE: 0 never, 1 when needed (default), 2 always
     int wmax = 0 /* auto */, threads = 0 /* auto */, force_global = 0, ens_group = 128;
     int smem_optin = 0, num_sms = 0;
@@ -891,6 +893,16 @@ static qap_status ensemble_tc(qap_ctx* c, uint32_t chain_begin, uint32_t chain_c
     k_reset<uint8_t, uint8_t><<<chain_count, 512, 0, c->stream>>>((const uint8_t*)c->dA, (const uint8_t*)c->dB,
                                                                    c->ens_p0, n, c->ld, c->tp, c->tbp, c->tst);
     CU(cudaGetLastError());
+    if (c->ens4 && e4_eligible(n)) {
+        // scratch phase four chains per SM (ens_chain.cuh): 128 TMEM columns and 160 threads per
+        // chain; more than a fifth of the shared memory per CTA caps an SM at the four chains
+        // whose 4 x 128 TMEM columns fill its 512
+        auto ks = n == 100 ? k_ens_scratch<100> : n == 50 ? k_ens_scratch<50> : n == 12 ? k_ens_scratch<12>
+                                                                                           : k_ens_scratch<0>;
+        const int ssm = std::max(e4_layout(n, c->ld).bytes, c->smem_optin / 5 + 1024);
+        CU(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, ssm));
+        ks<<<chain_count, E4_NT, ssm, c->stream>>>(a, c->tkout);
+    } else {
     auto ks = n == 100 ? k_sa_scratch<100, true> : n == 50 ? k_sa_scratch<50, true>
             : n == 12 ? k_sa_scratch<12, true> : k_sa_scratch<0, true>;
     // more than a third of the shared memory: at most two chains' CTAs per SM, whose 2 x 256 TMEM
@@ -898,6 +910,7 @@ static qap_status ensemble_tc(qap_ctx* c, uint32_t chain_begin, uint32_t chain_c
     const int ssm = std::max(sc_layout(c->ld).bytes, c->smem_optin / 3 + 1024);
     CU(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, ssm));
     ks<<<chain_count, tcs_nt<true>(), ssm, c->stream>>>(a, c->tkout);
+    }
     CU(cudaGetLastError());
     const int dt = 256, db = (c->M + dt - 1) / dt;
     for (uint32_t c0 = 0; c0 < chain_count; c0 += 65535u) {   // gridDim.y <= 65535: slices of chains
@@ -1102,6 +1115,10 @@ qap_status qap_set_option(qap_ctx* c, int32_t key, int64_t value) {
         case QAP_OPT_PROPOSAL:
             if (value != 0 && value != 1) return fail(c, QAP_E_INVALID_ARG, "proposal must be 0 or 1");
             c->proposal = (int)value;
+            return QAP_OK;
+        case QAP_OPT_ENSEMBLE_SCRATCH4:
+            if (value != 0 && value != 1) return fail(c, QAP_E_INVALID_ARG, "value must be 0 or 1");
+            c->ens4 = (int)value;
             return QAP_OK;
         case QAP_OPT_CLUSTER_ENGINE:
             if (value < 0 || value > 2) return fail(c, QAP_E_INVALID_ARG, "cluster engine must be 0, 1 or 2");

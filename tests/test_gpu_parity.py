@@ -746,3 +746,35 @@ def test_tmem_ensemble_more_chains_than_grid_y():
     per = res["per_chain"]
     for c in [0, 1, 65534, 65535, 65536]:
         _check_chain(per[c], A, B, O.start_perm(8, SA_SEED, c), c, I, sch, SA_SEED, follow)
+
+
+# ---------------- ensemble scratch phase, four chains per SM (ens_chain.cuh) ----------------
+
+@pytest.mark.parametrize("n,C,I", [(12, 64, 30000), (60, 40, 50000), (100, 24, 60000), (128, 10, 40000)])
+def test_ensemble_four_chains_per_sm_vs_two(n, C, I):
+    """QAP_OPT_ENSEMBLE_SCRATCH4 = 1 (default: G only in tensor memory, four chains per SM) and 0
+    (G and H, two chains per SM) give identical per-chain results, argmin and best permutation;
+    chains sampled against the oracle (followed at flagged near ties)."""
+    if n == 128:
+        rng = np.random.default_rng(5)
+        A = np.triu(rng.integers(0, 128, size=(n, n)), 1).astype(np.int32)
+        B = np.triu(rng.integers(0, 128, size=(n, n)), 1).astype(np.int32)
+        A, B = A + A.T, B + B.T
+    else:
+        A, B = taixxa(n, 70 + n)
+    p0s = start_perms(n, SA_SEED, 11, C)
+    sch = O.geometric_schedule_for(A, B, p0s[0], I)
+    out, fol = {}, {}
+    for e4 in (1, 0):
+        with Q.Solver(A, B, p0s[0]) as s:
+            assert s.uses_tensor_core()
+            s.set_option(Q.QAP_OPT_ENSEMBLE_SCRATCH4, e4)
+            out[e4] = s.ensemble(11, p0s, I, _sched(sch), SA_SEED, per_chain=True)
+            fol[e4] = _ens_follow(s)
+    assert fol[1] == fol[0]
+    assert (out[1]["best_cost"], out[1]["best_chain"]) == (out[0]["best_cost"], out[0]["best_chain"])
+    np.testing.assert_array_equal(out[1]["best_perm"], out[0]["best_perm"])
+    for i, (r1, r0) in enumerate(zip(out[1]["per_chain"], out[0]["per_chain"])):
+        assert r1 == r0, i
+    for i in sorted({0, 1, C - 1} | {c - 11 for c in fol[1]}):
+        _check_chain(out[1]["per_chain"][i], A, B, p0s[i], 11 + i, I, sch, SA_SEED, fol[1])
