@@ -247,10 +247,13 @@ typedef enum {
                                     B' and Δ distributed, N up to QAP_MAX_N): 1 (default) = only
                                     for chains no single SM holds (N > 256, 8-bit A); 2 = always
                                     (8-bit A, n >= 4); 0 = never.  Same trajectory either way. */
-    QAP_OPT_ENSEMBLE_SCRATCH4 = 11 /* tensor-memory ensembles: 1 (default) = the scratch phase of four
+    QAP_OPT_ENSEMBLE_SCRATCH4 = 11, /* tensor-memory ensembles: 1 (default) = the scratch phase of four
                                     chains per SM (G only in tensor memory, 128 columns; the window's
                                     rows of G exchanged through shared memory); 0 = two chains per
                                     SM (G and H).  Same results either way. */
+    QAP_OPT_SWITCH_GAP = 12      /* tensor-memory engine: the scratch phase hands over to the Δ engine
+                                    after this many iterations without an accept; 0 (default) =
+                                    4096 for single chains, 65536 for ensembles.  Same results. */
 } qap_option;
 qap_status qap_set_option(qap_ctx* ctx, int32_t key, int64_t value);
 /* 1 if the next qap_sa_run uses the tensor-memory engine (QAP_OPT_TENSOR_CORE), else 0. */

@@ -50,6 +50,7 @@ struct qap_ctx {
     bool delta_valid = false;
     bool sticky = false;
     std::string err;
+    long long switch_gap = 0;            // QAP_OPT_SWITCH_GAP (0 = engine default)
     int ens4 = 1;                        // QAP_OPT_ENSEMBLE_SCRATCH4: ensemble scratch phase 4 chains per SM
     int use_cluster = 1;                 // QAP_OPT_CLUSTER_ENGINE: 0 never, 1 when needed (default), 2 always
     int wmax = 0 /* auto */, threads = 0 /* auto */, force_global = 0, ens_group = 128;
@@ -588,7 +589,7 @@ qap_status qap_sa_run(qap_ctx* c, uint64_t k0, uint64_t iters, const qap_schedul
     a.ens = 0;
     a.dstride = 0;
     a.chain = 0u;
-    a.switch_gap = 0;
+    a.switch_gap = (unsigned long long)c->switch_gap;
     int launches = 0;
     if (tc) {
         a.wmax = c->wmax ? c->wmax : 1024;
@@ -884,7 +885,7 @@ static qap_status ensemble_tc(qap_ctx* c, uint32_t chain_begin, uint32_t chain_c
     a.theta = nullptr; a.theta_hdr = nullptr; a.theta_kb = a.theta_cnt = 0;
     // two scratch-phase chains share an SM but the Δ engine holds one: stay longer in the scratch
     // phase (config 5: gap 4096 / 16384 / 65536 / never = 3.67 / 3.64 / 3.62 / 3.66 s)
-    a.switch_gap = 65536;
+    a.switch_gap = c->switch_gap ? (unsigned long long)c->switch_gap : 65536ull;
     CU(cudaEventRecord(c->ev0, c->stream));
     if (!p0s) {                                  // chain-keyed start permutations on the device (R14b)
         k_start_perms<<<(chain_count + 127) / 128, 128, 0, c->stream>>>(n, seed, chain_begin, (int)chain_count, c->ens_p0);
@@ -1115,6 +1116,10 @@ qap_status qap_set_option(qap_ctx* c, int32_t key, int64_t value) {
         case QAP_OPT_PROPOSAL:
             if (value != 0 && value != 1) return fail(c, QAP_E_INVALID_ARG, "proposal must be 0 or 1");
             c->proposal = (int)value;
+            return QAP_OK;
+        case QAP_OPT_SWITCH_GAP:
+            if (value < 0 || value > 0x7FFFFFFFll) return fail(c, QAP_E_INVALID_ARG, "switch gap must be in [0, 2^31)");
+            c->switch_gap = value;
             return QAP_OK;
         case QAP_OPT_ENSEMBLE_SCRATCH4:
             if (value != 0 && value != 1) return fail(c, QAP_E_INVALID_ARG, "value must be 0 or 1");

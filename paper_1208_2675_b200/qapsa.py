@@ -28,6 +28,7 @@ QAP_OPT_RELABEL = 7
 QAP_OPT_RELABEL_CLUSTER = 8
 QAP_OPT_CLUSTER_ENGINE = 10
 QAP_OPT_ENSEMBLE_SCRATCH4 = 11
+QAP_OPT_SWITCH_GAP = 12
 QAP_OPT_PROPOSAL = 9
 QAP_ENGINE_SHARED_MEMORY, QAP_ENGINE_TENSOR_MEMORY, QAP_ENGINE_RELABEL, QAP_ENGINE_CLUSTER = 0, 1, 2, 3
 QAP_NEAR_LOG_CAP = 1024
