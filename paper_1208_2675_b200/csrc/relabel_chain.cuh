@@ -19,7 +19,7 @@
 // window; every twin before it is accepted, σ is rotated in one parallel step, and each twin
 // thread adds its accept to a private count and digest (R18 is a sum).
 //
-// Per cross accept (slots a < b), 1024 threads per CTA:
+// Per cross accept (slots a < b), 256 threads per CTA:
 //   window  one candidate per thread, decided by one shared-memory load of the exact integer
 //           threshold of its iteration (k_theta, theta_ring.cuh, R23; flagged iterations take the
 //           general float-θ / exact-double test)
@@ -47,7 +47,8 @@
 
 namespace qapsa {
 
-constexpr int RLB_NT = 1024;
+constexpr int RLB_NT = 256;     // one thread per window candidate (a window is <= 255 candidates)
+constexpr int RLB_NW = RLB_NT / 32;
 constexpr int RLB_MAXN = 256;
 constexpr int RLB_MAXCLS = 4;   // twin classes (>= 2 members) the relabel path handles
 #ifndef RLB_QB_EXP
@@ -337,13 +338,13 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
         }
         if (lane == 0) twm[warp] = tw;
         __syncthreads();
-        const int j = __reduce_min_sync(0xffffffffu, slots[lane].x);
+        const int j = __reduce_min_sync(0xffffffffu, lane < RLB_NW ? slots[lane].x : INT_MAX);
         parity ^= 1;
         const int cons = (j == INT_MAX) ? Wl : j + 1;
         // any twin among the consumed candidates (needs a barrier before σ is read again)
         const int lo = cons - 32 * lane;
         const unsigned below = lo >= 32 ? 0xffffffffu : (lo <= 0 ? 0u : ((1u << lo) - 1u));
-        const bool any_twin = __reduce_or_sync(0xffffffffu, twm[lane] & below) != 0u;
+        const bool any_twin = __reduce_or_sync(0xffffffffu, lane < RLB_NW ? twm[lane] & below : 0u) != 0u;
         if (near && t < cons && crank == 0) {             // R16: near ties of consumed iterations
             near_record(sink, k + (uint64_t)t, acc);
         }
@@ -379,8 +380,8 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
             stg[t] = 2 * (1024 * db + da);
             if (t != sa && t != sb) Dg[t] -= da * db;     // D''_v = D_v - dA_v dB_v (R10b)
         }
-        if (t >= 256 && t < 512) {                        // Z_a = A_a.B~_b, Z_b = A_b.B~_a (R10b)
-            const int i = t - 256;
+        {                                                 // Z_a = A_a.B~_b, Z_b = A_b.B~_a (R10b)
+            const int i = t;
             int za = 0, zb = 0;
             if (i < n) {
                 za = rlb_A(op1, sa, i) * rlb_B(op1, sb, i);
@@ -388,7 +389,7 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
             }
             za = __reduce_add_sync(0xffffffffu, za);
             zb = __reduce_add_sync(0xffffffffu, zb);
-            if (lane == 0) { zz[2 * (warp - 8)] = za; zz[2 * (warp - 8) + 1] = zb; }
+            if (lane == 0) { zz[2 * warp] = za; zz[2 * warp + 1] = zb; }
         }
         __syncthreads();
         const int ars = rlb_A(op1, sa, sb), brs = rlb_B(op1, sa, sb);
@@ -489,10 +490,16 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
         // canonical layout, so the 8 lanes of a quarter warp read 128 contiguous bytes): lane l
         // handles row v8 + (l & 7) and the 16-byte K chunks l / 8, + 4, + 8, + 12; the 4 partial
         // sums of a row are added with two shuffles.  Lane l (l < 8) keeps row v8 + l's entries.
-        int wa = -1, wb = -1, va = 0, vb = 0;
+        constexpr int NPASS = (RLB_MAXN + 7 + 8 * RLB_NW - 1) / (8 * RLB_NW);   // 8-row groups per warp
+        int wa[NPASS], wb[NPASS], va[NPASS], vb[NPASS];
+#pragma unroll
+        for (int ps_ = 0; ps_ < NPASS; ++ps_) { wa[ps_] = -1; wb[ps_] = -1; va[ps_] = 0; vb[ps_] = 0; }
         {
             const int rl = lane & 7, cq = lane >> 3;
-            for (int v8 = (vlo & ~7) + 8 * warp; v8 < vhi; v8 += RLB_NT / 4) {
+#pragma unroll
+            for (int pass = 0; pass < NPASS; ++pass) {
+                const int v8 = (vlo & ~7) + 8 * warp + pass * 8 * RLB_NW;
+                if (v8 >= vhi) break;
                 const int v = v8 + rl;
                 unsigned s8[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};   // Xa h/l, Xb h/l, Ya h/l, Yb h/l
 #pragma unroll
@@ -534,14 +541,17 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
                     const int fa = 2 * (xa + ars * db + yb - da * brs - Da - dv + 2 * av * bbv);
                     const int eb = v > sb ? rowaddr[sb] + v : rowaddr[v] + sb;
                     const int fb = 2 * (xb - ars * db + ya + da * brs - Db - dv + 2 * bv * abv);
-                    wa = ea; va = fa; wb = eb; vb = fb;   // (one pass per warp: rows <= 32 x 8)
+                    wa[pass] = ea; va[pass] = fa; wb[pass] = eb; vb[pass] = fb;
                 }
             }
         }
         __syncthreads();                                  // quads written: columns sa, sb next
-        if (wa >= 0) {                                    // this CTA computed them: store anywhere
-            dput(wa, va);
-            dput(wb, vb);
+#pragma unroll
+        for (int ps_ = 0; ps_ < NPASS; ++ps_) {
+            if (wa[ps_] >= 0) {                           // this CTA computed them: store anywhere
+                dput(wa[ps_], va[ps_]);
+                dput(wb[ps_], vb[ps_]);
+            }
         }
         if (t == RLB_NT - 1) dwr(rowaddr[sa] + sb, -dw);  // swapping back restores C
         __syncthreads();

@@ -50,7 +50,9 @@ def raw(rep):
 
 def main():
     tag = sys.argv[1]
-    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    outdir = os.environ.get("OUTDIR", os.path.join(ROOT, "profiles"))
+    os.makedirs(outdir, exist_ok=True)
+    path = os.path.join(outdir, "ncu_summary.json")
     try:
         summ = json.load(open(path))
         if "kernels" not in summ:
@@ -72,7 +74,7 @@ def main():
         summ["kernels"][kern] = d
         lines = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_lines.py"), rep, "25", str(units)],
                                capture_output=True, text=True).stdout
-        with open(os.path.join(ROOT, "profiles", f"{tag}_{kern}_ncu_summary.txt"), "w") as f:
+        with open(os.path.join(outdir, f"{tag}_{kern}_ncu_summary.txt"), "w") as f:
             f.write(f"{kern}: {d['capture']}\n")
             for k, v in d.items():
                 if k != "capture":
