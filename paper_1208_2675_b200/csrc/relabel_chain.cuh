@@ -61,10 +61,10 @@ constexpr int RLB_SBO = RLB_K / 16 * 128;        // 8-row group stride of the ca
 constexpr int RLB_BL = 256, RLB_AOFF = 512;      // K offsets of the Bl and A parts
 
 struct RlbLayout {
-    int op1, dsh, rowaddr, qdesc, pt, cls, sig, q, bestp, dg, stg, slots, twm, zz, flags, red,
+    int op1, dsh, rowaddr, qdesc, pt, cls, sig, q, bestp, dg, stg, slots, twm, ab, zz, flags, red,
         ring, tbar, bytes;
 };
-constexpr int RLB_RS = 8, RLB_RB = 256;          // threshold ring: 8 blocks of 256 (a window is <= 255)
+constexpr int RLB_RS = 4, RLB_RB = 256;          // threshold ring: 4 blocks of 256 (a window is <= 255)
 // quads of Δ~ owned by each CTA of a cluster of CL (quad g belongs to CTA g % CL)
 __host__ __device__ constexpr int rlb_share(int n, int CL) { return (quad_count(n) + CL - 1) / CL; }
 // CL = 1: Δ~ in global memory, all quad descriptors in shared memory; CL > 1: this CTA's share of
@@ -84,8 +84,9 @@ __host__ __device__ constexpr RlbLayout rlb_layout(int n, int CL = 1) {
     L.bestp = o;   o = align16(o + n * 2);
     L.dg = o;      o = align16(o + n * 4);
     L.stg = o;     o = align16(o + n4 * 4);
-    L.slots = o;   o = align16(o + 2 * 32 * 16);
-    L.twm = o;     o = align16(o + 2 * 32 * 4);
+    L.slots = o;   o = align16(o + 2 * RLB_NW * 16);
+    L.twm = o;     o = align16(o + 2 * RLB_NW * 4);
+    L.ab = o;      o = align16(o + RLB_MAXN * 8);         // stage: (A_a | A_b << 16, B~_a | B~_b << 16) per x
     L.zz = o;      o = align16(o + 16 * 4);
     L.flags = o;   o = align16(o + 4 * 4);
     L.red = o;     o = align16(o + 2 * 8);
@@ -162,6 +163,7 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
     int32_t* stg = reinterpret_cast<int32_t*>(smem + L.stg);   // 2 (1024 dB_x + dA_x)
     int4* slot_base = reinterpret_cast<int4*>(smem + L.slots);
     unsigned* twm_base = reinterpret_cast<unsigned*>(smem + L.twm);
+    uint2* abx = reinterpret_cast<uint2*>(smem + L.ab);
     int* zz = reinterpret_cast<int*>(smem + L.zz);
     int* flags = reinterpret_cast<int*>(smem + L.flags);
     unsigned long long* red = reinterpret_cast<unsigned long long*>(smem + L.red);
@@ -327,8 +329,8 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
                 }
             }
         }
-        int4* slots = slot_base + parity * 32;
-        unsigned* twm = twm_base + parity * 32;
+        int4* slots = slot_base + parity * RLB_NW;
+        unsigned* twm = twm_base + parity * RLB_NW;
         const unsigned bal = __ballot_sync(0xffffffffu, acc);
         const unsigned tw = __ballot_sync(0xffffffffu, twin);
         if (bal) {
@@ -375,17 +377,17 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
         // dA in [-255, 255], dB in [-65535, 65535] packed as 2 (1024 dB + dA): the difference of two
         // packed values is 2048 (dB_u - dB_v) + 2 (dA_u - dA_v) with |dA_u - dA_v| <= 510, so
         // hi = (d + 1024) >> 11 and lo2 = d - 2048 hi recover both and lo2 * hi is the rank term
-        if (t < n) {
-            const int da = rlb_A(op1, sa, t) - rlb_A(op1, sb, t), db = rlb_B(op1, sa, t) - rlb_B(op1, sb, t);
-            stg[t] = 2 * (1024 * db + da);
-            if (t != sa && t != sb) Dg[t] -= da * db;     // D''_v = D_v - dA_v dB_v (R10b)
-        }
-        {                                                 // Z_a = A_a.B~_b, Z_b = A_b.B~_a (R10b)
-            const int i = t;
-            int za = 0, zb = 0;
-            if (i < n) {
-                za = rlb_A(op1, sa, i) * rlb_B(op1, sb, i);
-                zb = rlb_A(op1, sb, i) * rlb_B(op1, sa, i);
+        {                                                 // x = t: the rows a, b of A and B~ at x once
+            int za = 0, zb = 0;                           // Z_a = A_a.B~_b, Z_b = A_b.B~_a (R10b)
+            if (t < n) {
+                const int aa = rlb_A(op1, sa, t), ab_ = rlb_A(op1, sb, t);
+                const int ba = rlb_B(op1, sa, t), bb = rlb_B(op1, sb, t);
+                const int da = aa - ab_, db = ba - bb;
+                stg[t] = 2 * (1024 * db + da);
+                if (t != sa && t != sb) Dg[t] -= da * db; // D''_v = D_v - dA_v dB_v (R10b)
+                za = aa * bb;
+                zb = ab_ * ba;
+                abx[t] = make_uint2((uint32_t)aa | ((uint32_t)ab_ << 16), (uint32_t)ba | ((uint32_t)bb << 16));
             }
             za = __reduce_add_sync(0xffffffffu, za);
             zb = __reduce_add_sync(0xffffffffu, zb);
@@ -490,6 +492,12 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
         // canonical layout, so the 8 lanes of a quarter warp read 128 contiguous bytes): lane l
         // handles row v8 + (l & 7) and the 16-byte K chunks l / 8, + 4, + 8, + 12; the 4 partial
         // sums of a row are added with two shuffles.  Lane l (l < 8) keeps row v8 + l's entries.
+        // touching entries (R10b) of this CTA's rows v in [vlo, vhi) on the CUDA cores: the four
+        // dot products X_a = B~_v.A_a, X_b, Y_a = A_v.B~_a, Y_b by dp4a over the byte planes
+        // B~ = 256 Bh + Bl and A.  A warp pass takes 8 rows v8 .. v8 + 7 (one 8-row group of the
+        // canonical layout, so the 8 lanes of a quarter warp read 128 contiguous bytes): lane l
+        // handles row v8 + (l & 7) and the 16-byte K chunks l / 8, + 4, + 8, + 12; the 4 partial
+        // sums of a row are added with two shuffles and lane l < 8 keeps row v8 + l's entries.
         constexpr int NPASS = (RLB_MAXN + 7 + 8 * RLB_NW - 1) / (8 * RLB_NW);   // 8-row groups per warp
         int wa[NPASS], wb[NPASS], va[NPASS], vb[NPASS];
 #pragma unroll
@@ -532,16 +540,16 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
                     const int xb = (int)(s8[2] * 256u + s8[3]);    // X_b = B~_v.A_b
                     const int ya = (int)(s8[4] * 256u + s8[5]);    // Y_a = A_v.B~_a
                     const int yb = (int)(s8[6] * 256u + s8[7]);    // Y_b = A_v.B~_b
-                    const int av = rlb_A(op1, sa, v), bv = rlb_A(op1, sb, v);
-                    const int abv = rlb_B(op1, sa, v), bbv = rlb_B(op1, sb, v);
+                    const uint2 abv_ = abx[v];                     // the stage's A_a, A_b, B~_a, B~_b at v
+                    const int av = (int)(abv_.x & 0xFFFFu), bv = (int)(abv_.x >> 16);
+                    const int abv = (int)(abv_.y & 0xFFFFu), bbv = (int)(abv_.y >> 16);
                     const int da = av - bv, db = abv - bbv;
                     const int dv = Dg[v];                 // D''_v (updated in the stage)
                     // R10b: δ''(a,v) and δ''(b,v) from pre-swap rows
-                    const int ea = v > sa ? rowaddr[sa] + v : rowaddr[v] + sa;
-                    const int fa = 2 * (xa + ars * db + yb - da * brs - Da - dv + 2 * av * bbv);
-                    const int eb = v > sb ? rowaddr[sb] + v : rowaddr[v] + sb;
-                    const int fb = 2 * (xb - ars * db + ya + da * brs - Db - dv + 2 * bv * abv);
-                    wa[pass] = ea; va[pass] = fa; wb[pass] = eb; vb[pass] = fb;
+                    wa[pass] = v > sa ? rowaddr[sa] + v : rowaddr[v] + sa;
+                    va[pass] = 2 * (xa + ars * db + yb - da * brs - Da - dv + 2 * av * bbv);
+                    wb[pass] = v > sb ? rowaddr[sb] + v : rowaddr[v] + sb;
+                    vb[pass] = 2 * (xb - ars * db + ya + da * brs - Db - dv + 2 * bv * abv);
                 }
             }
         }
