@@ -467,16 +467,16 @@ def ensemble_roofline(e, peaks, sms):
     algo = BYTES_PER_PROPOSAL * props + bytes_per_accept(e["n"]) * res.accepted
     peak, src, _ = smem_peak(e["clocks"], peaks, sms=sms * ws)
     achieved = algo / (e["kern_ms"] / 1e3) / 1e9
-    prof = profile_summary("ensemble")
+    prof = profile_summary("k_ens_scratch")
     hbm = None
     if prof.get("dram_bytes_per_launch"):
-        gbs = prof["dram_bytes_per_launch"] / (prof["launch_ms"] / 1e3) / 1e9 if prof.get("launch_ms") else None
+        gbs = prof["dram_bytes_per_launch"] / (prof["time_ms"] / 1e3) / 1e9 if prof.get("time_ms") else None
         hbm = {"dram_gbs": gbs, "peak_gbs": peaks.get("hbm_gbs", 6538.6),
                "frac": gbs / peaks.get("hbm_gbs", 6538.6) if gbs else None,
-               "source": prof.get("source")}
+               "source": prof.get("capture")}
     return {"bound": "smem", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": prof.get("dram_bytes_per_launch"),
-            "kernel": "k_sa_scratch + k_sa_tc (ensemble launches)", "kernel_ms": e["kern_ms"],
+            "kernel": "k_ens_scratch + k_sa_tc (ensemble launches)", "kernel_ms": e["kern_ms"],
             "peak_source": src, "algorithmic_bytes_per_launch": algo,
             "accepted": res.accepted, "chain_iterations": props, "hbm": hbm, "ncu": prof or None}
 
@@ -546,7 +546,7 @@ def run_ours(args):
                 "metric": METRIC_N, "value": C * I * 1e3 / ens["step_ms"], "unit": UNIT_N,
                 "ms_per_step": ens["step_ms"], "kernel_ms": ens["kern_ms"],
                 "value_kernel_only": C * I * 1e3 / ens["kern_ms"],
-                "engine": "tensor-memory: k_start_perms, k_reset, k_sa_scratch, k_delta_init, k_sa_tc "
+                "engine": "tensor-memory: k_start_perms, k_reset, k_ens_scratch (4 chains per SM), k_delta_init, k_sa_tc "
                           "over all chains, then k_ens_collect + k_ens_reduce and the NCCL min-reduce",
                 "config": {"workload": "config5 ensemble: 8192 chains x N=100 tai100a-shaped x 1e7 iterations",
                            "chains": C, "iters_per_chain": I, "n": n,
