@@ -562,8 +562,10 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
             }
         }
         if (t == RLB_NT - 1) dwr(rowaddr[sa] + sb, -dw);  // swapping back restores C
-        __syncthreads();
-        if (CL > 1) { cl_arrive(); pend_wait = true; }    // this CTA's update written
+        // this CTA's update written: on a cluster the split barrier orders the stores before the
+        // next window's reads (its wait comes first there); on one SM a CTA barrier does
+        if (CL > 1) { cl_arrive(); pend_wait = true; }
+        else __syncthreads();
         pa = sa;
         pb = sb;
         k = kacc + 1;
