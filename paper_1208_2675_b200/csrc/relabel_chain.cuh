@@ -273,8 +273,8 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
                     *rb_ = v;
                 }
             }
-            if (warp == 1) {                              // rows pa, pb (Bh and Bl), word-wise
-                for (int w = lane; w < 2 * RLB_BL / 4; w += 32) {
+            {                                             // rows pa, pb (Bh and Bl), word-wise
+                for (int w = t; w < 2 * RLB_BL / 4; w += RLB_NT) {
                     const int kk = 4 * w, c = kk & 255;
                     uint32_t m = 0;
                     if ((unsigned)(pa - c) < 4u) m |= 0xFFu << (8 * (pa - c));
@@ -510,18 +510,23 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
                 if (v8 >= vhi) break;
                 const int v = v8 + rl;
                 unsigned s8[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};   // Xa h/l, Xb h/l, Ya h/l, Yb h/l
+                // row bases of the canonical layout; K chunk c of row x is at base_x + 128 c
+                const uint8_t* pv = op1 + rlb_off(v, 16 * cq);
+                const uint8_t* pa_ = op1 + rlb_off(sa, 16 * cq);
+                const uint8_t* pb_ = op1 + rlb_off(sb, 16 * cq);
+                constexpr int CH = 128, CA = RLB_AOFF / 16 * 128, CL_ = RLB_BL / 16 * 128;
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                    const int kc = 16 * (cq + 4 * i);
-                    const uint4 Av = *reinterpret_cast<const uint4*>(op1 + rlb_off(v, RLB_AOFF + kc));
-                    const uint4 Hv = *reinterpret_cast<const uint4*>(op1 + rlb_off(v, kc));
-                    const uint4 Lv = *reinterpret_cast<const uint4*>(op1 + rlb_off(v, RLB_BL + kc));
-                    const uint4 Aa = *reinterpret_cast<const uint4*>(op1 + rlb_off(sa, RLB_AOFF + kc));
-                    const uint4 Ab = *reinterpret_cast<const uint4*>(op1 + rlb_off(sb, RLB_AOFF + kc));
-                    const uint4 Ha = *reinterpret_cast<const uint4*>(op1 + rlb_off(sa, kc));
-                    const uint4 La = *reinterpret_cast<const uint4*>(op1 + rlb_off(sa, RLB_BL + kc));
-                    const uint4 Hb = *reinterpret_cast<const uint4*>(op1 + rlb_off(sb, kc));
-                    const uint4 Lb = *reinterpret_cast<const uint4*>(op1 + rlb_off(sb, RLB_BL + kc));
+                    const int o = 4 * i * CH;
+                    const uint4 Av = *reinterpret_cast<const uint4*>(pv + CA + o);
+                    const uint4 Hv = *reinterpret_cast<const uint4*>(pv + o);
+                    const uint4 Lv = *reinterpret_cast<const uint4*>(pv + CL_ + o);
+                    const uint4 Aa = *reinterpret_cast<const uint4*>(pa_ + CA + o);
+                    const uint4 Ab = *reinterpret_cast<const uint4*>(pb_ + CA + o);
+                    const uint4 Ha = *reinterpret_cast<const uint4*>(pa_ + o);
+                    const uint4 La = *reinterpret_cast<const uint4*>(pa_ + CL_ + o);
+                    const uint4 Hb = *reinterpret_cast<const uint4*>(pb_ + o);
+                    const uint4 Lb = *reinterpret_cast<const uint4*>(pb_ + CL_ + o);
                     auto dot = [](uint4 x, uint4 y, unsigned c) {
                         return __dp4a(x.x, y.x, __dp4a(x.y, y.y, __dp4a(x.z, y.z, __dp4a(x.w, y.w, c))));
                     };
