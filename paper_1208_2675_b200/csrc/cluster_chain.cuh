@@ -177,9 +177,9 @@ __global__ void __cluster_dims__(CLC, 1, 1) __launch_bounds__(CLC_NT, 1) k_sa_cl
         int Wl = win_f(Rw, L0, m1);
         if ((uint32_t)Wl > kr_end - kr) Wl = (int)(kr_end - kr);
         const int ko = kofs0 + (int)kr;
-        if (t == 0 && (ko >> 10) != ring_blo) {
+        if ((ko >> 10) != ring_blo) {     // a block passed (warp-uniform test; one thread refills)
             ring_blo = ko >> 10;
-            TR.refill(k0 + kr);
+            if (t == 0) TR.refill(k0 + kr);
         }
         if (ko + Wl > ring_hi) {
             TR.ensure_ofs(ko + Wl);

@@ -293,9 +293,9 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
 
         {   // thresholds of the window's iterations resident (theta_ring.cuh)
             const int ko = (int)(k - TR.kb);
-            if (t == 0 && (ko >> 8) != ring_blo) {
+            if ((ko >> 8) != ring_blo) {      // a block passed (warp-uniform test; one thread refills)
                 ring_blo = ko >> 8;
-                TR.refill(k);
+                if (t == 0) TR.refill(k);
             }
             if (ko + Wl > ring_hi) {
                 TR.ensure_ofs(ko + Wl);

@@ -235,9 +235,9 @@ __global__ void __launch_bounds__(tcs_nt<ENS>(), ENS ? 2 : 1) k_sa_scratch(const
         const int Wl = wg.Wl;
         if (RING) {
             const int ko = kofs0 + (int)kr;
-            if (t == 0 && (ko >> 10) != ring_blo) {   // a block passed: its slot can be refilled
+            if ((ko >> 10) != ring_blo) {     // a block passed: its slot can be refilled (uniform test)
                 ring_blo = ko >> 10;
-                TR.refill(k0 + kr);
+                if (t == 0) TR.refill(k0 + kr);
             }
             if (ko + Wl > ring_hi) {             // blocks not yet known complete
                 TR.ensure_ofs(ko + Wl);

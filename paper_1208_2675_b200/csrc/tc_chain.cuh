@@ -302,6 +302,7 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
     const int wcap = RING ? min(a.wscan, TCK_WSCAN) : a.wscan;
     int W = wcap;
     int parity = 0;
+    int ring_blo = -1, ring_hi = 0;              // ring: last block refilled from, offsets known resident
     // certain-reject bound: δ > 38.5 T32(k) >= 38.4 T_kk gives exp(-δ/T) < 2^-54 <= r (chain.cuh);
     // rounded up to an integer, so the exact test below also sees every δ <= 38.5 T32(k)
     int rejI = rej_bound(sch, k);
@@ -325,9 +326,16 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
             const uint64_t remaining = k_end - k;
             if ((uint64_t)Wl > remaining) Wl = (int)remaining;
         }
-        if (RING) {
-            if (t == 0) TR.refill(k);
-            TR.ensure(k + (uint64_t)Wl);
+        if (RING) {                              // thresholds of the window resident (theta_ring.cuh)
+            const int ko = (int)(k - TR.kb);
+            if ((ko >> 10) != ring_blo) {        // a block passed (warp-uniform test; one thread refills)
+                ring_blo = ko >> 10;
+                if (t == 0) TR.refill(k);
+            }
+            if (ko + Wl > ring_hi) {
+                TR.ensure_ofs(ko + Wl);
+                ring_hi = (int)(TR.ready * TH_BLK);
+            }
         }
         int4* sl = slots + parity * TCK_NW;
         int best_o = INT_MAX, best_d = 0, best_rs = 0;
