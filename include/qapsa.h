@@ -240,8 +240,11 @@ typedef enum {
     QAP_OPT_PROPOSAL = 9,        /* candidate order: 0 (default) = the sequential cyclic
                                     enumeration (R4); 1 = random pairs, iteration k proposes pair
                                     index floor(x M / 2^32), x = Philox(seed; k, chain, tag 3)
-                                    (R22); runs on the shared-memory kernel (single chain and
-                                    qap_ensemble_run) */
+                                    (R22); single chains on the tensor-memory Δ engine where the
+                                    instance allows it (a window = 256 random candidates whose Δ
+                                    cells are gathered from their TMEM lanes; no scratch phase),
+                                    else on the shared-memory kernel; qap_ensemble_run on the
+                                    shared-memory kernel */
     QAP_OPT_CLUSTER_ENGINE = 10, /* cluster engine (f1; one chain spread over the
                                     shared memory of a thread-block cluster of 8 SMs, rows of A,
                                     B' and Δ distributed, N up to QAP_MAX_N): 1 (default) = only

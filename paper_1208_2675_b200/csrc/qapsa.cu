@@ -146,9 +146,11 @@ static std::vector<unsigned char> compact(int n, int ld, const int32_t* X) {
     return out;
 }
 
+// single chains: sequential (R4) or random (R22) proposals; ensembles: sequential only
 static bool use_tc_engine(const qap_ctx* c) {
-    return c->tc_ok && c->use_tc && !c->force_global && c->proposal == 0;
+    return c->tc_ok && c->use_tc && !c->force_global;
 }
+static bool use_tc_ensemble(const qap_ctx* c) { return use_tc_engine(c) && c->proposal == 0; }
 
 static int dab_bytes(const qap_ctx* c) { return (c->ta == 1 && c->tb == 1) ? 4 : 8; }
 
@@ -594,13 +596,15 @@ qap_status qap_sa_run(qap_ctx* c, uint64_t k0, uint64_t iters, const qap_schedul
     if (tc) {
         a.wmax = c->wmax ? c->wmax : 1024;
         // compile-time problem size for the BASELINE configurations, generic otherwise
-        auto kern = c->n == 100 ? k_sa_tc<100> : c->n == 50 ? k_sa_tc<50> : c->n == 12 ? k_sa_tc<12> : k_sa_tc<0>;
+        // random proposals (R22): the Δ engine with gathered windows, no scratch phase
+        auto kern = c->proposal ? k_sa_tc<0, false, true>
+                  : c->n == 100 ? k_sa_tc<100> : c->n == 50 ? k_sa_tc<50> : c->n == 12 ? k_sa_tc<12> : k_sa_tc<0>;
         CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         auto ks = c->n == 100 ? k_sa_scratch<100> : c->n == 50 ? k_sa_scratch<50>
                 : c->n == 12 ? k_sa_scratch<12> : k_sa_scratch<0>;
         const int ssm = sc_layout(c->ld).bytes;
         CU(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, ssm));
-        bool scratch = c->use_scratch != 0;
+        bool scratch = c->use_scratch != 0 && c->proposal == 0;
         // chunks of TH_CHUNK iterations: θ of the chunk on the whole GPU, then the chain kernels
         for (uint64_t kc = k0; kc < k0 + iters; kc += TH_CHUNK) {
             const uint64_t ke = std::min<uint64_t>(k0 + iters, kc + TH_CHUNK);
@@ -712,7 +716,7 @@ qap_status qap_sa_run(qap_ctx* c, uint64_t k0, uint64_t iters, const qap_schedul
     CU(cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1));
     c->last_scratch_ms = 0.f;
     c->last_scratch[0] = c->last_scratch[1] = 0;
-    if (tc && c->use_scratch) {
+    if (tc && c->use_scratch && c->proposal == 0) {
         CU(cudaEventElapsedTime(&c->last_scratch_ms, c->ev0, c->evm));
         CU(cudaMemcpy(c->last_scratch, c->dkout, sizeof c->last_scratch, cudaMemcpyDeviceToHost));
     }
@@ -974,7 +978,7 @@ qap_status qap_ensemble_run(qap_ctx* c, uint32_t chain_begin, uint32_t chain_cou
     if (p0s)
         for (uint32_t i = 0; i < chain_count; ++i)
             if (!is_perm(n, p0s + (size_t)i * n)) return fail(c, QAP_E_DIMENSION, "a start permutation is invalid");
-    if (use_tc_engine(c))
+    if (use_tc_ensemble(c))
         return ensemble_tc(c, chain_begin, chain_count, p0s, iters, sch, seed, best_cost, best_chain,
                            best_perm, sum_stats, per_chain);
     const int nt = (c->ta == 1 && c->tb == 1) ? c->ens_group : 128;

@@ -70,7 +70,7 @@ __host__ __device__ __forceinline__ int cofs(int x, int k) {
 }
 
 struct TcLayout {
-    int a, b, rd, rg, rh, tmp, p, pinv, bestp, rowr, rows, xbuf, zbuf, slots, thm, misc, tbar, thdr, bytes;
+    int a, b, rd, rg, rh, tmp, p, pinv, bestp, rowr, rows, xbuf, zbuf, slots, thm, misc, tbar, thdr, rnd, bytes;
 };
 // ld: row stride of A and B (row_stride(n, true) <= 144)
 __host__ __device__ inline TcLayout tc_layout(int ld) {
@@ -95,6 +95,7 @@ __host__ __device__ inline TcLayout tc_layout(int ld) {
     L.misc = o;  o += 64;                       // mbarriers (2 x 8 B) | TMEM base (4 B)
     L.tbar = o;  o += TH_SLOTS_TC * 8;          // threshold ring mbarriers
     L.thdr = o;  o += TH_SLOTS_TC * 16;         // threshold ring block headers
+    L.rnd = o;   o += 64 + 2 * 4 * TCK_NT * 2 + TCK_NT * 8;   // random proposals: lists, pairs, gathered Δ
     L.bytes = o;
     return L;
 }
@@ -189,7 +190,10 @@ __device__ __noinline__ int tc_exact(int d, uint64_t kk, Sched sch, uint64_t see
     return (acc ? 1 : 0) | (near ? 2 : 0);
 }
 
-template <int NFIX, bool ENS = false>
+// RND: random proposals (R22): iteration k proposes pair index floor(x M / 2^32),
+// x = Philox(seed; k, chain, tag 3); a window is the next TCK_NT iterations, one candidate per
+// thread, its Δ cells gathered from their TMEM lanes by the warps owning them
+template <int NFIX, bool ENS = false, bool RND = false>
 __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
     constexpr bool RING = !ENS;                  // single chain: precomputed θ (theta_ring.cuh)
     extern __shared__ __align__(16) unsigned char smem[];
@@ -287,6 +291,7 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
         reinterpret_cast<int*>(smem + L.tmp), reinterpret_cast<int4*>(smem + L.thdr),
         reinterpret_cast<uint64_t*>(smem + L.tbar), a.theta, a.theta_hdr, a.theta_kb, a.theta_cnt, k);
     if (RING && t == 0 && k < a.k_end) TR.start(k);
+    if (RND && t < 8) reinterpret_cast<int*>(smem + L.rnd)[t] = 0;   // random windows: list lengths
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
@@ -321,7 +326,7 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
         TCT_MARK(pt0, u0 + v0);
         const int L0 = n - v0, m1 = n - 1 - u0;
         const int R = win_rows_whole(n, u0, L0, m1, W);
-        int Wl = win_f(R, L0, m1);
+        int Wl = RND ? TCK_NT : win_f(R, L0, m1);
         {
             const uint64_t remaining = k_end - k;
             if ((uint64_t)Wl > remaining) Wl = (int)remaining;
@@ -343,46 +348,183 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
         // groups of 8 rows u0 + 8g .. u0 + 8g + 7, g = warp / 4, + 2, ...: thread v reads its cells
         // Δ_{u, v} (columns u) with one tcgen05.ld; offsets grow with the row, so a warp stops after
         // its first group holding an accept (every later candidate comes after it)
-        const int NG = (R + 7) >> 3;
-        // exact integer thresholds (R23) unless a block of the window is flagged or the window is
-        // cut short by the end of the call: the general path below
-        const int2 sp = RING ? TR.span(k, k + (uint64_t)Wl) : make_int2(1, 0);
-        if (!sp.x && Wl == win_f(R, L0, m1)) {
-            // thread v's candidates: rows [ulo, uhi] (row u0 from column v0 on, u < v)
-            const int ulo = v >= v0 ? u0 : u0 + 1;
-            const int uhi = vin ? min(v - 1, u0 + R - 1) : -1;
-            const int kofs = (int)(k - TR.kb);
+        if (RND) {
+            // ---------------- random window: candidate c = t at iteration k + c ----------------
+            int* gcnt = reinterpret_cast<int*>(smem + L.rnd);                 // [2][4] list lengths
+            uint16_t* glist = reinterpret_cast<uint16_t*>(smem + L.rnd + 64);  // [2][4][TCK_NT]
+            uint16_t* cuv = glist + 2 * 4 * TCK_NT;                            // [TCK_NT] u | v << 8 ... as 2 x u16
+            int* dval = reinterpret_cast<int*>(cuv + 2 * TCK_NT);               // [TCK_NT] gathered Δ_uv
+            if (t < 4) gcnt[(parity ^ 1) * 4 + t] = 0;   // the next window's lists (this parity's were reset before)
+            int cu = 0, cvv = 1;
+            const bool cex = t < Wl;
+            if (cex) {
+                const int idx = proposal_index(true, 0, 0, M, k + (uint64_t)t, seed, cv.chain);
+                tri_pair(n, idx, &cu, &cvv);
+                cuv[2 * t] = (uint16_t)cu;
+                cuv[2 * t + 1] = (uint16_t)cvv;
+                const int qd = cvv >> 5;         // the lane quadrant holding cell (lane v, column u)
+                const int pos = atomicAdd(&gcnt[parity * 4 + qd], 1);
+                glist[(parity * 4 + qd) * TCK_NT + pos] = (uint16_t)t;
+            }
+            tc::fence_before_sync();
+            __syncthreads();
+            tc::fence_after_sync();
+            {   // gather: warps q and q + 4 read their quadrant's cells, 8 columns per tcgen05.ld batch
+                const int qd = warp & 3;
+                const int cnt = gcnt[parity * 4 + qd];
+                const uint16_t* gl = glist + (parity * 4 + qd) * TCK_NT;
+                for (int e0 = 8 * (warp >> 2); e0 < cnt; e0 += 16) {
+                    uint32_t vals[8];
+                    int cs[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        cs[i] = e0 + i < cnt ? (int)gl[e0 + i] : -1;
+                        const int col = cs[i] >= 0 ? (int)cuv[2 * cs[i]] : 0;
+                        tc::tmem_ld1(tm + quad_lane + (uint32_t)col, vals[i]);
+                    }
+                    tc::tmem_wait_ld();
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        if (cs[i] < 0) continue;
+                        const int u_ = cuv[2 * cs[i]], v_ = cuv[2 * cs[i] + 1];
+                        if (lane == (v_ & 31)) {
+                            int d = (int)vals[i];
+                            if (v_ == pend_r) d = rowR[u_];      // cells still being patched
+                            else if (v_ == pend_s) d = rowS[u_];
+                            dval[cs[i]] = d;
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+            if (cex) {
+                const int d = dval[t];
+                bool acc;
+                const int thr = TR.at_ofs((int)(k - TR.kb) + t);
+                if (thr >= 0 || d <= 0) {
+                    acc = d <= thr || d <= 0;    // R23; δ <= 0 accepted (R5)
+                } else {                         // flagged iteration: general test (R16)
+                    float th, m;
+                    theta_of(sch, seed, cv.chain, k + (uint64_t)t, &th, &m);
+                    const float df = (float)d;
+                    acc = df < th - m;
+                    if (!acc && !(df > th + m)) {
+                        const int x = tc_exact(d, k + (uint64_t)t, sch, seed, cv.chain);
+                        acc = x & 1;
+                        if (x & 2) { nt_o[0] = t; nt_d[0] = acc; }
+                    }
+                }
+                if (acc) {
+                    best_o = t;
+                    best_d = d;
+                    best_rs = cu | (cvv << 8) | ((int)p[cu] << 16) | ((int)p[cvv] << 24);
+                }
+            }
+        } else {
+            const int NG = (R + 7) >> 3;
+            // exact integer thresholds (R23) unless a block of the window is flagged or the window is
+            // cut short by the end of the call: the general path below
+            const int2 sp = RING ? TR.span(k, k + (uint64_t)Wl) : make_int2(1, 0);
+            if (!sp.x && Wl == win_f(R, L0, m1)) {
+                // thread v's candidates: rows [ulo, uhi] (row u0 from column v0 on, u < v)
+                const int ulo = v >= v0 ? u0 : u0 + 1;
+                const int uhi = vin ? min(v - 1, u0 + R - 1) : -1;
+                const int kofs = (int)(k - TR.kb);
+                for (int g = warp >> 2; g < NG; g += 2) {
+                    const int i0 = 8 * g;
+                    int f = i0 == 0 ? 0 : win_f(i0, L0, m1);   // offset of row u0 + i0's first candidate
+                    uint32_t dd[8];
+                    tc::tmem_ld8(tm + quad_lane + (uint32_t)(u0 + i0), dd);
+                    const int lo = ulo - u0 - i0, hi = uhi - u0 - i0;   // this thread's rows i in [lo, hi]
+                    tc::tmem_wait_ld();
+                    if (v == pend_r || v == pend_s) {    // cells still being patched: their new values
+                        const int* row = v == pend_r ? rowR : rowS;
+    #pragma unroll
+                        for (int i = 0; i < 8; ++i)
+                            if (u0 + i0 + i < v) dd[i] = (uint32_t)row[u0 + i0 + i];
+                    }
+                    int mn = INT_MAX;                // smallest δ of the thread's candidates
+    #pragma unroll
+                    for (int i = 0; i < 8; ++i) mn = min(mn, (i >= lo && i <= hi) ? (int)dd[i] : INT_MAX);
+                    unsigned am = 0;
+                    int oo[8];
+                    if (__any_sync(0xffffffffu, mn <= sp.y)) {   // else every candidate is above every threshold
+    #pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            const int ii = i0 + i;
+                            const int first = ii == 0 ? v0 : u0 + ii + 1;
+                            oo[i] = f - first + v;
+                            f += ii == 0 ? L0 : m1 - ii;
+                            const int thr = TR.ring[(kofs + oo[i]) & (TR.RING - 1)];
+                            am |= (unsigned)(i >= lo && i <= hi && (int)dd[i] <= thr) << i;
+                        }
+                    }
+                    if (__any_sync(0xffffffffu, am != 0)) {
+                        if (am) {                    // this thread's first accepted candidate
+                            const int i = __ffs(am) - 1;
+                            const int u = u0 + i0 + i;
+                            best_o = oo[i];
+                            best_d = (int)dd[i];
+                            best_rs = u | (v << 8) | ((int)p[u] << 16) | (px << 24);
+                        }
+                        break;
+                    }
+                }
+            } else
             for (int g = warp >> 2; g < NG; g += 2) {
                 const int i0 = 8 * g;
                 int f = i0 == 0 ? 0 : win_f(i0, L0, m1);   // offset of row u0 + i0's first candidate
+                if (f >= Wl) break;                  // warp-uniform: the group starts past the window
                 uint32_t dd[8];
-                tc::tmem_ld8(tm + quad_lane + (uint32_t)(u0 + i0), dd);
-                const int lo = ulo - u0 - i0, hi = uhi - u0 - i0;   // this thread's rows i in [lo, hi]
+                tc::tmem_ld8(tm + quad_lane + (uint32_t)(u0 + i0), dd);   // columns u0+i0 .. (< 140: inside G, unused)
                 tc::tmem_wait_ld();
                 if (v == pend_r || v == pend_s) {    // cells still being patched: their new values
                     const int* row = v == pend_r ? rowR : rowS;
-#pragma unroll
+    #pragma unroll
                     for (int i = 0; i < 8; ++i)
                         if (u0 + i0 + i < v) dd[i] = (uint32_t)row[u0 + i0 + i];
                 }
-                int mn = INT_MAX;                // smallest δ of the thread's candidates
-#pragma unroll
-                for (int i = 0; i < 8; ++i) mn = min(mn, (i >= lo && i <= hi) ? (int)dd[i] : INT_MAX);
-                unsigned am = 0;
+                // per candidate: exists / accepted outright (δ <= 0, R5) / needs the threshold test
+                unsigned need = 0, am = 0;
                 int oo[8];
-                if (__any_sync(0xffffffffu, mn <= sp.y)) {   // else every candidate is above every threshold
-#pragma unroll
+    #pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int ii = i0 + i;
+                    const int first = ii == 0 ? v0 : u0 + ii + 1;
+                    oo[i] = f - first + v;
+                    f += ii == 0 ? L0 : m1 - ii;
+                    const int d = (int)dd[i];
+                    const bool ex = ii < R && v >= first && vin && oo[i] < Wl;
+                    am |= (unsigned)(ex && d <= 0) << i;
+                    need |= (unsigned)(ex && d > 0 && d <= rejI) << i;   // above rejI: certain reject
+                }
+                if (__any_sync(0xffffffffu, need != 0)) {
+                    const int pnk = pk == k ? pn : 0;
+    #pragma unroll
                     for (int i = 0; i < 8; ++i) {
-                        const int ii = i0 + i;
-                        const int first = ii == 0 ? v0 : u0 + ii + 1;
-                        oo[i] = f - first + v;
-                        f += ii == 0 ? L0 : m1 - ii;
-                        const int thr = TR.ring[(kofs + oo[i]) & (TR.RING - 1)];
-                        am |= (unsigned)(i >= lo && i <= hi && (int)dd[i] <= thr) << i;
+                        if ((need >> i) & 1u) {
+                            const int o = oo[i];
+                            const int d = (int)dd[i];
+                            float th, m;
+                            if (!RING && o < pnk) { const float2 q = thm[o]; th = q.x; m = q.y; }
+                            else theta_of(sch, seed, cv.chain, k + (uint64_t)o, &th, &m);
+                            const float df = (float)d;
+                            bool ac = df < th - m;
+                            if (!ac && !(df > th + m)) {  // inside the margin: exact double test (R16)
+                                const int x = tc_exact(d, k + (uint64_t)o, sch, seed, cv.chain);
+                                ac = x & 1;
+                                if (x & 2) {          // near tie: logged after the decision if consumed
+                                    const int e = nt_o[0] == INT_MAX ? 0 : 1;
+                                    if (nt_o[e] == INT_MAX) { nt_o[e] = o; nt_d[e] = ac; }
+                                    else near_record(sink, k + (uint64_t)o, ac);   // a third (never seen): logged eagerly
+                                }
+                            }
+                            am |= (unsigned)ac << i;
+                        }
                     }
                 }
                 if (__any_sync(0xffffffffu, am != 0)) {
-                    if (am) {                    // this thread's first accepted candidate
+                    if (am) {                        // this thread's first accepted candidate
                         const int i = __ffs(am) - 1;
                         const int u = u0 + i0 + i;
                         best_o = oo[i];
@@ -391,69 +533,6 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
                     }
                     break;
                 }
-            }
-        } else
-        for (int g = warp >> 2; g < NG; g += 2) {
-            const int i0 = 8 * g;
-            int f = i0 == 0 ? 0 : win_f(i0, L0, m1);   // offset of row u0 + i0's first candidate
-            if (f >= Wl) break;                  // warp-uniform: the group starts past the window
-            uint32_t dd[8];
-            tc::tmem_ld8(tm + quad_lane + (uint32_t)(u0 + i0), dd);   // columns u0+i0 .. (< 140: inside G, unused)
-            tc::tmem_wait_ld();
-            if (v == pend_r || v == pend_s) {    // cells still being patched: their new values
-                const int* row = v == pend_r ? rowR : rowS;
-#pragma unroll
-                for (int i = 0; i < 8; ++i)
-                    if (u0 + i0 + i < v) dd[i] = (uint32_t)row[u0 + i0 + i];
-            }
-            // per candidate: exists / accepted outright (δ <= 0, R5) / needs the threshold test
-            unsigned need = 0, am = 0;
-            int oo[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int ii = i0 + i;
-                const int first = ii == 0 ? v0 : u0 + ii + 1;
-                oo[i] = f - first + v;
-                f += ii == 0 ? L0 : m1 - ii;
-                const int d = (int)dd[i];
-                const bool ex = ii < R && v >= first && vin && oo[i] < Wl;
-                am |= (unsigned)(ex && d <= 0) << i;
-                need |= (unsigned)(ex && d > 0 && d <= rejI) << i;   // above rejI: certain reject
-            }
-            if (__any_sync(0xffffffffu, need != 0)) {
-                const int pnk = pk == k ? pn : 0;
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    if ((need >> i) & 1u) {
-                        const int o = oo[i];
-                        const int d = (int)dd[i];
-                        float th, m;
-                        if (!RING && o < pnk) { const float2 q = thm[o]; th = q.x; m = q.y; }
-                        else theta_of(sch, seed, cv.chain, k + (uint64_t)o, &th, &m);
-                        const float df = (float)d;
-                        bool ac = df < th - m;
-                        if (!ac && !(df > th + m)) {  // inside the margin: exact double test (R16)
-                            const int x = tc_exact(d, k + (uint64_t)o, sch, seed, cv.chain);
-                            ac = x & 1;
-                            if (x & 2) {          // near tie: logged after the decision if consumed
-                                const int e = nt_o[0] == INT_MAX ? 0 : 1;
-                                if (nt_o[e] == INT_MAX) { nt_o[e] = o; nt_d[e] = ac; }
-                                else near_record(sink, k + (uint64_t)o, ac);   // a third (never seen): logged eagerly
-                            }
-                        }
-                        am |= (unsigned)ac << i;
-                    }
-                }
-            }
-            if (__any_sync(0xffffffffu, am != 0)) {
-                if (am) {                        // this thread's first accepted candidate
-                    const int i = __ffs(am) - 1;
-                    const int u = u0 + i0 + i;
-                    best_o = oo[i];
-                    best_d = (int)dd[i];
-                    best_rs = u | (v << 8) | ((int)p[u] << 16) | (px << 24);
-                }
-                break;
             }
         }
         {
@@ -478,9 +557,11 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
         if (j == INT_MAX) {                      // no accepted swap in the window
             TCT_ACC(1, pt0, j);
             k += (uint64_t)Wl;
-            u0 += R;                             // whole rows: the cursor moves to the next row
-            v0 = u0 + 1;
-            if (u0 >= n - 1) { u0 = 0; v0 = 1; }
+            if (!RND) {
+                u0 += R;                         // whole rows: the cursor moves to the next row
+                v0 = u0 + 1;
+                if (u0 >= n - 1) { u0 = 0; v0 = 1; }
+            }
             W = min(2 * W, wcap);
             rejI = rej_bound(sch, k);
             continue;

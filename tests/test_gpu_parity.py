@@ -544,16 +544,26 @@ def test_qaplib_fixture_through_the_abi():
 
 # ---------------- f4: random proposals (R22) ----------------
 
-@pytest.mark.parametrize("n,I", [(5, 20000), (12, 100000), (50, 300000), (100, 200000)])
-def test_random_proposals_single_chain(n, I):
-    """R22 random proposals (QAP_OPT_PROPOSAL = 1) on the shared-memory engine: bit-exact
+@pytest.mark.parametrize("tc", [1, 0])
+@pytest.mark.parametrize("n,I", [(5, 20000), (12, 100000), (50, 300000), (100, 200000), (128, 100000)])
+def test_random_proposals_single_chain(n, I, tc):
+    """R22 random proposals (QAP_OPT_PROPOSAL = 1) on the tensor-memory Δ engine (windows of 256
+    random candidates gathered from their TMEM lanes) and on the shared-memory engine: bit-exact
     against the oracle's random-proposal mode, split into uneven calls."""
-    A, B = taixxa(n, 1000 + n)
+    if n == 128:
+        rng = np.random.default_rng(9)
+        A = np.triu(rng.integers(0, 128, size=(n, n)), 1).astype(np.int32)
+        B = np.triu(rng.integers(0, 128, size=(n, n)), 1).astype(np.int32)
+        A, B = A + A.T, B + B.T
+    else:
+        A, B = taixxa(n, 1000 + n)
     p0 = start_perm(n, SA_SEED, 0)
+    opts = [(Q.QAP_OPT_PROPOSAL, 1), (TC, tc)]
     with Q.Solver(A, B, p0) as s:
-        s.set_option(Q.QAP_OPT_PROPOSAL, 1)
-        assert s.engine() == Q.QAP_ENGINE_SHARED_MEMORY
-    _compare_run(A, B, p0, I, O.geometric_schedule_for(A, B, p0, I), opts=[(Q.QAP_OPT_PROPOSAL, 1)],
+        for k_, v_ in opts:
+            s.set_option(k_, v_)
+        assert s.engine() == (Q.QAP_ENGINE_TENSOR_MEMORY if tc else Q.QAP_ENGINE_SHARED_MEMORY)
+    _compare_run(A, B, p0, I, O.geometric_schedule_for(A, B, p0, I), opts=opts,
                  k_splits=[0, 7, I // 3, I], proposal=1)
 
 
