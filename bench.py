@@ -333,7 +333,7 @@ def single_chain(args, Q, local, stream, pg, ws):
             s2.run(0, I, sch, SA_SEED)
             s2.state(want_delta=False)
         e2e_ms.append(1e3 * (time.perf_counter() - t))
-    e2e_t = statistics.mean(e2e_ms)
+    e2e_t = statistics.median(e2e_ms)
     if pg:
         t = torch.tensor([e2e_t], device="cuda", dtype=torch.float64)
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
@@ -701,7 +701,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--dry-run", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--e2e-steps", type=int, default=3, help="end-to-end steps (median reported)")
     ap.add_argument("--no-ensemble", action="store_true")
     ap.add_argument("--no-single", action="store_true", help="N > 1: skip the nested single chain")
     ap.add_argument("--ens-chains", type=int, default=8192)

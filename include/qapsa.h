@@ -219,8 +219,10 @@ typedef enum {
     QAP_OPT_ENSEMBLE_GROUP = 4,  /* threads per chain in qap_ensemble_run: 64, 128 or 256 */
     QAP_OPT_TENSOR_CORE = 5,     /* qap_sa_run engine: 1 (default) = Δ in tensor memory with the
                                     rank update on the tensor cores when the instance allows it
-                                    (4 <= n <= 128, all entries <= 127), else the shared-memory
-                                    kernel; 0 = always the shared-memory kernel */
+                                    (4 <= n <= 128, all entries <= 127) and proposals are
+                                    sequential, else the shared-memory kernel; 2 = also for random
+                                    proposals (R22; slower than the shared-memory kernel); 0 =
+                                    always the shared-memory kernel */
     QAP_OPT_SCRATCH_PHASE = 6,   /* tensor-memory engine only: 1 (default) = run the high-acceptance
                                     start of each qap_sa_run without Δ (δ from G = A B'^T, SURVEY
                                     f2) until no swap is accepted for 4096 iterations, then rebuild
@@ -240,11 +242,10 @@ typedef enum {
     QAP_OPT_PROPOSAL = 9,        /* candidate order: 0 (default) = the sequential cyclic
                                     enumeration (R4); 1 = random pairs, iteration k proposes pair
                                     index floor(x M / 2^32), x = Philox(seed; k, chain, tag 3)
-                                    (R22); single chains on the tensor-memory Δ engine where the
-                                    instance allows it (a window = 256 random candidates whose Δ
-                                    cells are gathered from their TMEM lanes; no scratch phase),
-                                    else on the shared-memory kernel; qap_ensemble_run on the
-                                    shared-memory kernel */
+                                    (R22); the shared-memory kernel (single chain and
+                                    qap_ensemble_run), or with QAP_OPT_TENSOR_CORE = 2 the
+                                    tensor-memory Δ engine (windows of up to 256 random candidates
+                                    whose Δ cells are gathered from their TMEM lanes) */
     QAP_OPT_CLUSTER_ENGINE = 10, /* cluster engine (f1; one chain spread over the
                                     shared memory of a thread-block cluster of 8 SMs, rows of A,
                                     B' and Δ distributed, N up to QAP_MAX_N): 1 (default) = only

@@ -146,9 +146,11 @@ static std::vector<unsigned char> compact(int n, int ld, const int32_t* X) {
     return out;
 }
 
-// single chains: sequential (R4) or random (R22) proposals; ensembles: sequential only
+// single chains: sequential proposals (R4); random ones (R22) only when forced
+// (QAP_OPT_TENSOR_CORE = 2: measured slower than the shared-memory engine, config 3: 2.0e7 vs
+// 6.0e7 it/s); ensembles: sequential only
 static bool use_tc_engine(const qap_ctx* c) {
-    return c->tc_ok && c->use_tc && !c->force_global;
+    return c->tc_ok && c->use_tc && !c->force_global && (c->proposal == 0 || c->use_tc == 2);
 }
 static bool use_tc_ensemble(const qap_ctx* c) { return use_tc_engine(c) && c->proposal == 0; }
 
@@ -332,8 +334,11 @@ qap_status qap_create(int32_t n, const int32_t* A, const int32_t* B, const int32
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
         return fail(nullptr, QAP_E_CUDA, "no CUDA device (libqapsa has no CPU fallback)");
     if (device < 0 || device >= ndev) return fail(nullptr, QAP_E_INVALID_ARG, "bad device ordinal");
-    cudaDeviceProp prop;
-    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major < 10)
+    // three attributes (cudaGetDeviceProperties queries them all and costs milliseconds per call)
+    int major = 0, smem_optin = 0, num_sms = 0;
+    if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device) != cudaSuccess || major < 10 ||
+        cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device) != cudaSuccess ||
+        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess)
         return fail(nullptr, QAP_E_CUDA, "device is not sm_100 (Blackwell)");
 
     c = new qap_ctx();
@@ -345,12 +350,12 @@ qap_status qap_create(int32_t n, const int32_t* A, const int32_t* B, const int32
     c->ta = maxA <= 255 ? 1 : 2;
     c->tb = maxB <= 255 ? 1 : 2;
     c->tc_ok = tc_eligible(n, maxA, maxB);
-    c->smem_optin = (int)prop.sharedMemPerBlockOptin;
+    c->smem_optin = smem_optin;
     std::vector<int32_t> hrow;
     std::vector<uint16_t> hq;
     quad_tables(n, &hrow, &hq);
     c->nqt = (int)hq.size();
-    c->num_sms = prop.multiProcessorCount;
+    c->num_sms = num_sms;
     if (cudaSetDevice(device) != cudaSuccess) {
         delete c;
         return fail(nullptr, QAP_E_CUDA, "cudaSetDevice failed");
@@ -1108,7 +1113,8 @@ qap_status qap_set_option(qap_ctx* c, int32_t key, int64_t value) {
             c->force_global = value ? 1 : 0;
             return QAP_OK;
         case QAP_OPT_TENSOR_CORE:
-            c->use_tc = value ? 1 : 0;
+            if (value < 0 || value > 2) return fail(c, QAP_E_INVALID_ARG, "tensor core must be 0, 1 or 2");
+            c->use_tc = (int)value;
             return QAP_OK;
         case QAP_OPT_SCRATCH_PHASE:
             c->use_scratch = value ? 1 : 0;

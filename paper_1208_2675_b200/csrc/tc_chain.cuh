@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
     tri_pair(n, (int)(k % (uint64_t)M), &u0, &v0);
     // window cap: the ring (TH_SLOTS_TC blocks) keeps its prefetch ahead of a whole window
     const int wcap = RING ? min(a.wscan, TCK_WSCAN) : a.wscan;
-    int W = wcap;
+    int W = RND ? 32 : wcap;
     int parity = 0;
     int ring_blo = -1, ring_hi = 0;              // ring: last block refilled from, offsets known resident
     // certain-reject bound: δ > 38.5 T32(k) >= 38.4 T_kk gives exp(-δ/T) < 2^-54 <= r (chain.cuh);
@@ -326,7 +326,7 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
         TCT_MARK(pt0, u0 + v0);
         const int L0 = n - v0, m1 = n - 1 - u0;
         const int R = win_rows_whole(n, u0, L0, m1, W);
-        int Wl = RND ? TCK_NT : win_f(R, L0, m1);
+        int Wl = RND ? min(W, TCK_NT) : win_f(R, L0, m1);   // random: W candidates (adaptive, <= one per thread)
         {
             const uint64_t remaining = k_end - k;
             if ((uint64_t)Wl > remaining) Wl = (int)remaining;
@@ -719,7 +719,7 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
             pn = (int)min((uint64_t)TCK_TH, k_end - kacc - 1);   // thresholds the helpers prepared
             u0 = nu0;
             v0 = nv0;
-            W = max(64, min(wcap, round_up32(8 * (j + 1))));
+            W = RND ? max(32, min(TCK_NT, round_up32(4 * (j + 1)))) : max(64, min(wcap, round_up32(8 * (j + 1))));
         }
         ++accepted;
         k = kacc + 1;

@@ -39,7 +39,7 @@ constexpr int TH_SLOTS = 8;                      // scratch phase: ring blocks (
 constexpr int TH_RING = TH_BLK * TH_SLOTS;
 constexpr int TH_RING_BYTES = TH_RING * 4;
 constexpr int TH_SLOTS_TC = 32;                  // Δ engine (windows up to 7 blocks): 128 KB
-constexpr unsigned long long TH_CHUNK = 1ull << 27;   // iterations per threshold buffer fill (512 MB)
+constexpr unsigned long long TH_CHUNK = 1ull << 24;   // iterations per threshold buffer fill (64 MB)
 
 // thr_k and its flag (R23): the decision of metropolis() at every integer next to θ_k
 __device__ __forceinline__ int exact_threshold(const Sched& sch, uint64_t seed, uint32_t chain, uint64_t k,

@@ -544,11 +544,12 @@ def test_qaplib_fixture_through_the_abi():
 
 # ---------------- f4: random proposals (R22) ----------------
 
-@pytest.mark.parametrize("tc", [1, 0])
+@pytest.mark.parametrize("tc", [2, 1, 0])
 @pytest.mark.parametrize("n,I", [(5, 20000), (12, 100000), (50, 300000), (100, 200000), (128, 100000)])
 def test_random_proposals_single_chain(n, I, tc):
-    """R22 random proposals (QAP_OPT_PROPOSAL = 1) on the tensor-memory Δ engine (windows of 256
-    random candidates gathered from their TMEM lanes) and on the shared-memory engine: bit-exact
+    """R22 random proposals (QAP_OPT_PROPOSAL = 1) on the tensor-memory Δ engine (QAP_OPT_TENSOR_CORE
+    = 2: windows of random candidates gathered from their TMEM lanes) and on the shared-memory
+    engine (the default for random proposals, 1, and 0): bit-exact
     against the oracle's random-proposal mode, split into uneven calls."""
     if n == 128:
         rng = np.random.default_rng(9)
@@ -562,7 +563,7 @@ def test_random_proposals_single_chain(n, I, tc):
     with Q.Solver(A, B, p0) as s:
         for k_, v_ in opts:
             s.set_option(k_, v_)
-        assert s.engine() == (Q.QAP_ENGINE_TENSOR_MEMORY if tc else Q.QAP_ENGINE_SHARED_MEMORY)
+        assert s.engine() == (Q.QAP_ENGINE_TENSOR_MEMORY if tc == 2 else Q.QAP_ENGINE_SHARED_MEMORY)
     _compare_run(A, B, p0, I, O.geometric_schedule_for(A, B, p0, I), opts=opts,
                  k_splits=[0, 7, I // 3, I], proposal=1)
 

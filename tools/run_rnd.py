@@ -9,7 +9,7 @@ from qap_inputs import SA_SEED, config  # noqa: E402
 
 I = int(float(sys.argv[1])) if len(sys.argv) > 1 else 10**7
 A, B, p0, cfg = config(3)
-for tc in (1, 0):
+for tc in (2, 0):
     s = Q.Solver(A, B, p0)
     s.set_option(Q.QAP_OPT_PROPOSAL, 1)
     s.set_option(Q.QAP_OPT_TENSOR_CORE, tc)
