@@ -515,6 +515,18 @@ def test_cluster_engine_large_n(n):
     assert acc > 1000
 
 
+@pytest.mark.parametrize("n", [257, 263])
+def test_cluster_engine_ragged_n(n):
+    """N not a multiple of the cluster (rows of the last CTAs shorter), 8-bit B, five calls."""
+    A, B = taixxa(n, 500 + n)
+    p0 = start_perm(n, 21, 0)
+    I = 50000
+    with Q.Solver(A, B, p0) as s:
+        assert s.engine() == Q.QAP_ENGINE_CLUSTER
+    sch = O.geometric_schedule_for(A, B, p0, I)
+    _compare_run(A, B, p0, I, sch, mode=O.MODE_SCRATCH, k_splits=[0, 1, 999, 20000, 33333, I])
+
+
 def test_cluster_engine_uint16_b():
     """16-bit B on the cluster engine (N = 300 > 256, entries up to 2000)."""
     n = 300
@@ -644,7 +656,8 @@ def _near_tie_setup(n=12, inst=3, seed=SA_SEED, chain=0, I=5000):
 
 
 NEAR_ENGINES = ENGINES + [pytest.param([(TC, 0), (RLB, 3)], id="relabel"),
-                          pytest.param([(TC, 0), (RLB, 3), (RLBC, 1)], id="relabel_1sm")]
+                          pytest.param([(TC, 0), (RLB, 3), (RLBC, 1)], id="relabel_1sm"),
+                          pytest.param([(Q.QAP_OPT_CLUSTER_ENGINE, 2)], id="cluster")]
 
 
 @pytest.mark.parametrize("engine", NEAR_ENGINES)
