@@ -337,14 +337,16 @@ __global__ void __launch_bounds__(tcs_nt<ENS>(), ENS ? 2 : 1) k_sa_scratch(const
             const int bd = a0 ? dd[0] : dd[1];
             const int brs = (u0 + h2 + (a0 ? 0 : 1)) | (v << 8) | ((a0 ? pu[0] : pu[1]) << 16) | (px << 24);
             const int wmin = __reduce_min_sync(0xffffffffu, best_o);
-            if (best_o == wmin && (wmin != INT_MAX || lane == 0)) sl[warp] = make_int4(best_o, bd, brs, 0);
+            // slot key = offset << 3 | warp: the CTA minimum names its slot (no ballot afterwards)
+            if (best_o == wmin && (wmin != INT_MAX || lane == 0))
+                sl[warp] = make_int4(wmin == INT_MAX ? INT_MAX : (wmin << 3) | warp, bd, brs, 0);
         }
         TCT_ACC(1, pt0, acc_mask);
         // probe the previous update MMA now: the stage then waits only if it is still running
         const bool mma_done = !mma_pending || tc::mbar_test(mbar, ph);
         group_sync(4, 32 * TCS_RW);              // window decision
-        const int tv = lane < TCS_RW ? sl[lane].x : INT_MAX;
-        const int j = __reduce_min_sync(0xffffffffu, tv);
+        const int jkey = __reduce_min_sync(0xffffffffu, lane < TCS_RW ? sl[lane].x : INT_MAX);
+        const int j = jkey == INT_MAX ? INT_MAX : jkey >> 3;
         TCT_MARK(pt1, j);
         TCT_ACC(10, pt0, j);
         parity ^= 1;
@@ -366,8 +368,7 @@ __global__ void __launch_bounds__(tcs_nt<ENS>(), ENS ? 2 : 1) k_sa_scratch(const
             fresh = true;
             continue;
         }
-        const unsigned bw = __ballot_sync(0xffffffffu, tv == j);
-        const int4 win = sl[__ffs(bw) - 1];
+        const int4 win = sl[jkey & 7];
         const int dw = win.y;
         const int r = win.z & 0xFF, s = (win.z >> 8) & 0xFF;
         const int pr = (win.z >> 16) & 0xFF, ps = (int)((unsigned)win.z >> 24);
