@@ -256,11 +256,13 @@ __global__ void __launch_bounds__(E4_NT, 4) k_ens_scratch(const ChainArgs a, uns
                 best_rs = ac ? ((u0 + i) | (v << 8) | (pu[i] << 16) | (px << 24)) : best_rs;
             }
             const int wmin = __reduce_min_sync(0xffffffffu, best_o);
-            if (best_o == wmin && (wmin != INT_MAX || lane == 0)) sl[warp] = make_int4(best_o, best_d, best_rs, 0);
+            // slot key = offset << 2 | warp: the CTA minimum names its slot (no ballot afterwards)
+            if (best_o == wmin && (wmin != INT_MAX || lane == 0))
+                sl[warp] = make_int4(wmin == INT_MAX ? INT_MAX : (wmin << 2) | warp, best_d, best_rs, 0);
         }
         group_sync(4, 128);                      // window decision
-        const int tv = lane < 4 ? sl[lane].x : INT_MAX;
-        const int j = __reduce_min_sync(0xffffffffu, tv);
+        const int jkey = __reduce_min_sync(0xffffffffu, lane < 4 ? sl[lane].x : INT_MAX);
+        const int j = jkey == INT_MAX ? INT_MAX : jkey >> 2;
         parity ^= 1;
         if (near_mask) {                         // R16: log near ties of consumed iterations
             const int consumed = (j == INT_MAX) ? Wl : j + 1;
@@ -276,8 +278,7 @@ __global__ void __launch_bounds__(E4_NT, 4) k_ens_scratch(const ChainArgs a, uns
             W = min(2 * W, wmax);
             continue;
         }
-        const unsigned bw = __ballot_sync(0xffffffffu, tv == j);
-        const int4 win = sl[__ffs(bw) - 1];
+        const int4 win = sl[jkey & 3];
         const int dw = win.y;
         const int r = win.z & 0xFF, s = (win.z >> 8) & 0xFF;
         const int pr = (win.z >> 16) & 0xFF, ps = (int)((unsigned)win.z >> 24);

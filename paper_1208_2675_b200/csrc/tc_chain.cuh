@@ -537,15 +537,17 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
         }
         {
             const int wmin = __reduce_min_sync(0xffffffffu, best_o);
-            if (best_o == wmin && (wmin != INT_MAX || lane == 0)) sl[warp] = make_int4(best_o, best_d, best_rs, 0);
+            // slot key = offset << 3 | warp: the CTA minimum names its slot (no ballot afterwards)
+            if (best_o == wmin && (wmin != INT_MAX || lane == 0))
+                sl[warp] = make_int4(wmin == INT_MAX ? INT_MAX : (wmin << 3) | warp, best_d, best_rs, 0);
         }
         TCT_ACC(10, pt0, best_o);
         tc::fence_before_sync();
         __syncthreads();
         tc::fence_after_sync();
         pend_r = pend_s = -1;                    // the helpers' patch is complete
-        const int tv = lane < TCK_NW ? sl[lane].x : INT_MAX;
-        const int j = __reduce_min_sync(0xffffffffu, tv);
+        const int jkey = __reduce_min_sync(0xffffffffu, lane < TCK_NW ? sl[lane].x : INT_MAX);
+        const int j = jkey == INT_MAX ? INT_MAX : jkey >> 3;
         TCT_MARK(pt1, j);
         parity ^= 1;
         if (nt_o[0] != INT_MAX) {                // R16: log near ties of consumed iterations
@@ -566,8 +568,7 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
             rejI = rej_bound(sch, k);
             continue;
         }
-        const unsigned bw = __ballot_sync(0xffffffffu, tv == j);
-        const int4 win = sl[__ffs(bw) - 1];
+        const int4 win = sl[jkey & 7];
         const int dw = win.y;
         const int r = win.z & 0xFF, s = (win.z >> 8) & 0xFF;    // r < s
         const int pr = (win.z >> 16) & 0xFF, ps = (int)((unsigned)win.z >> 24);
