@@ -329,16 +329,61 @@ __global__ void __cluster_dims__(CLC, 1, 1) __launch_bounds__(CLC_NT, 1) k_sa_cl
             const uint8_t* av = Arow + (size_t)lx * lda;
             const TB* bv = Brow + (size_t)lx * lda;   // post-swap row v
             int sr = 0, ss = 0;
-            for (int k = lane; k < n; k += 32) {
-                const int kp = k == r ? s : k == s ? r : k;
-                const int bvk = (int)bv[k];
-                if (k != r && k != v) sr += ((int)ar[k] - (int)av[k]) * (bvk - (int)bs[kp]);
-                if (k != s && k != v) ss += ((int)as[k] - (int)av[k]) * (bvk - (int)br[kp]);
-            }
+            if constexpr (sizeof(TB) == 1) {
+                // 8-bit rows: the sums over all k as byte dot products (dp4a, 16 k per lane; the
+                // rows are zero past n), then the exchange of columns r, s in B'_r, B'_s and the
+                // excluded terms k = r | s and k = v as exact scalar corrections (lane 0)
+                unsigned P[7] = {0u, 0u, 0u, 0u, 0u, 0u, 0u};
+                for (int k0 = 16 * lane; k0 < lda; k0 += 512) {
+                    const uint4 Ar = *reinterpret_cast<const uint4*>(ar + k0);
+                    const uint4 As_ = *reinterpret_cast<const uint4*>(as + k0);
+                    const uint4 Av = *reinterpret_cast<const uint4*>(av + k0);
+                    const uint4 Bv = *reinterpret_cast<const uint4*>(bv + k0);
+                    const uint4 Bs_ = *reinterpret_cast<const uint4*>(bs + k0);
+                    const uint4 Br_ = *reinterpret_cast<const uint4*>(br + k0);
+                    auto dot = [](uint4 x, uint4 y, unsigned c) {
+                        return __dp4a(x.x, y.x, __dp4a(x.y, y.y, __dp4a(x.z, y.z, __dp4a(x.w, y.w, c))));
+                    };
+                    P[0] = dot(Ar, Bv, P[0]);    // a_r . b'_v
+                    P[1] = dot(Ar, Bs_, P[1]);   // a_r . (pre-swap row s)
+                    P[2] = dot(Av, Bv, P[2]);    // a_v . b'_v
+                    P[3] = dot(Av, Bs_, P[3]);   // a_v . (pre-swap row s)
+                    P[4] = dot(As_, Bv, P[4]);   // a_s . b'_v
+                    P[5] = dot(As_, Br_, P[5]);  // a_s . (pre-swap row r)
+                    P[6] = dot(Av, Br_, P[6]);   // a_v . (pre-swap row r)
+                }
 #pragma unroll
-            for (int sh = 16; sh > 0; sh >>= 1) {
-                sr += __shfl_xor_sync(0xffffffffu, sr, sh);
-                ss += __shfl_xor_sync(0xffffffffu, ss, sh);
+                for (int e = 0; e < 7; ++e) P[e] = __reduce_add_sync(0xffffffffu, P[e]);
+                if (lane == 0) {
+                    auto g = [](const uint8_t* x, int k) { return (int)x[k]; };
+                    const int arr = g(ar, r), ars_ = g(ar, s), asr = g(as, r), ass = g(as, s);
+                    const int avr = g(av, r), avs = g(av, s), avv = g(av, v), arv = g(ar, v), asv = g(as, v);
+                    const int bvr = (int)bv[r], bvs = (int)bv[s], bvv = (int)bv[v];
+                    const int bsr = (int)bs[r], bss = (int)bs[s], bsv = (int)bs[v];
+                    const int brr = (int)br[r], brs = (int)br[s], brv = (int)br[v];
+                    // post-swap rows r, s of B': bs, br with columns r and s exchanged
+                    const int P1 = (int)P[1] - arr * bsr - ars_ * bss + arr * bss + ars_ * bsr;
+                    const int P3 = (int)P[3] - avr * bsr - avs * bss + avr * bss + avs * bsr;
+                    const int P5 = (int)P[5] - asr * brr - ass * brs + asr * brs + ass * brr;
+                    const int P6 = (int)P[6] - avr * brr - avs * brs + avr * brs + avs * brr;
+                    // sum over every k, minus k = r and k = v (δ''(r, v)); k = s and k = v (δ''(s, v))
+                    sr = (int)P[0] - P1 - (int)P[2] + P3 - (arr - avr) * (bvr - bss) - (arv - avv) * (bvv - bsv);
+                    ss = (int)P[4] - P5 - (int)P[2] + P6 - (ass - avs) * (bvs - brr) - (asv - avv) * (bvv - brv);
+                }
+                ss = __shfl_sync(0xffffffffu, ss, 0);
+                sr = __shfl_sync(0xffffffffu, sr, 0);
+            } else {
+                for (int k = lane; k < n; k += 32) {
+                    const int kp = k == r ? s : k == s ? r : k;
+                    const int bvk = (int)bv[k];
+                    if (k != r && k != v) sr += ((int)ar[k] - (int)av[k]) * (bvk - (int)bs[kp]);
+                    if (k != s && k != v) ss += ((int)as[k] - (int)av[k]) * (bvk - (int)br[kp]);
+                }
+#pragma unroll
+                for (int sh = 16; sh > 0; sh >>= 1) {
+                    sr += __shfl_xor_sync(0xffffffffu, sr, sh);
+                    ss += __shfl_xor_sync(0xffffffffu, ss, sh);
+                }
             }
             if (lane < 2) {                      // δ''(r, v) by lane 0, δ''(s, v) by lane 1
                 const int x = lane == 0 ? r : s;
