@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(E4_NT, 4) k_ens_scratch(const ChainArgs a, uns
         const int jkey = __reduce_min_sync(0xffffffffu, lane < 4 ? sl[lane].x : INT_MAX);
         const int j = jkey == INT_MAX ? INT_MAX : jkey >> 2;
         parity ^= 1;
-        if (near_mask) {                         // R16: log near ties of consumed iterations
+        if (__any_sync(0xffffffffu, near_mask != 0)) {   // R16: log near ties of consumed iterations (uniform test)
             const int consumed = (j == INT_MAX) ? Wl : j + 1;
 #pragma unroll
             for (int i = 0; i < 4; ++i) {

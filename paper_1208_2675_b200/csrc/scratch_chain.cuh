@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(tcs_nt<ENS>(), ENS ? 2 : 1) k_sa_scratch(const
         TCT_MARK(pt1, j);
         TCT_ACC(10, pt0, j);
         parity ^= 1;
-        if (near_mask) {                         // R16: log near ties of consumed iterations
+        if (__any_sync(0xffffffffu, near_mask != 0)) {   // R16: log near ties of consumed iterations (uniform test)
             const int consumed = (j == INT_MAX) ? Wl : j + 1;
 #pragma unroll
             for (int e = 0; e < 2; ++e) {

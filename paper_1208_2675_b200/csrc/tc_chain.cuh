@@ -550,7 +550,7 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
         const int j = jkey == INT_MAX ? INT_MAX : jkey >> 3;
         TCT_MARK(pt1, j);
         parity ^= 1;
-        if (nt_o[0] != INT_MAX) {                // R16: log near ties of consumed iterations
+        if (__any_sync(0xffffffffu, nt_o[0] != INT_MAX)) {   // R16: log near ties of consumed iterations
             const int consumed = (j == INT_MAX) ? Wl : j + 1;
 #pragma unroll
             for (int e = 0; e < 2; ++e)
