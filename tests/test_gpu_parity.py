@@ -802,3 +802,14 @@ def test_ensemble_four_chains_per_sm_vs_two(n, C, I):
         assert r1 == r0, i
     for i in sorted({0, 1, C - 1} | {c - 11 for c in fol[1]}):
         _check_chain(out[1]["per_chain"][i], A, B, p0s[i], 11 + i, I, sch, SA_SEED, fol[1])
+
+
+@pytest.mark.parametrize("gap", [1, 64, 100000, 2**31 - 1])
+def test_switch_gap_invariance(gap):
+    """QAP_OPT_SWITCH_GAP moves the scratch -> Δ hand-over (f2) without changing the trajectory:
+    bit-exact against the oracle for a gap of 1 (hand over at once), 64, 1e5 and never."""
+    A, B = taixxa(60, 66)
+    p0 = start_perm(60, 6, 0)
+    I = 150000
+    sch = O.geometric_schedule_for(A, B, p0, I)
+    _compare_run(A, B, p0, I, sch, opts=[(Q.QAP_OPT_SWITCH_GAP, gap)], k_splits=[0, 50001, I])
