@@ -51,16 +51,23 @@ struct ClLayout {
 // R = ceil(n / CLC) owned rows; lda = row stride of the A / B' rows (elements, multiple of 16)
 __host__ __device__ inline int clc_rows(int n) { return (n + CLC - 1) / CLC; }
 __host__ __device__ inline int clc_lda(int n) { return (n + 15) & ~15; }
-// owned Δ entries of CTA c (rows x = c, c + CLC, ... < n - 1): sum of (n - 1 - x)
+// Δ row x is kept quad-aligned: entries v in [b(x), n4), b(x) = 4 floor((x + 1) / 4), n4 = n
+// rounded up to 4 (the cells v <= x and v >= n are padding, never read), so that the disjoint
+// update runs on 16-byte quads like the single-SM engines' quad layout (§5)
+__host__ __device__ inline int clc_n4(int n) { return (n + 3) & ~3; }
+__host__ __device__ inline int clc_b(int x) { return (x + 1) & ~3; }
+// owned Δ cells of CTA c (rows x = c, c + CLC, ...): sum of (n4 - b(x))
 __host__ __device__ inline int clc_dcount(int n, int c) {
     int e = 0;
-    for (int x = c; x < n - 1; x += CLC) e += n - 1 - x;
+    for (int x = c; x < CLC * clc_rows(n); x += CLC) e += max(0, clc_n4(n) - clc_b(x));
     return e;
 }
-// offset of row x's first entry in its owner's Δ rows: rows q CLC + (x mod CLC), q < x / CLC
+// offset of row x's first cell (column b(x)) in its owner's Δ rows: rows j CLC + c, j < x / CLC
+// (CLC = 8: b(8 j + c) = 8 j + 4 floor((c + 1) / 4))
 __host__ __device__ inline int clc_doff(int n, int x) {
+    static_assert(CLC == 8, "closed form for clusters of 8");
     const int q = x / CLC, c = x % CLC;
-    return q * (n - 1 - c) - CLC * (q * (q - 1) / 2);
+    return q * (clc_n4(n) - 4 * ((c + 1) / 4)) - CLC * (q * (q - 1) / 2);
 }
 __host__ __device__ inline ClLayout cl_layout(int n, int tb) {
     ClLayout L;
@@ -128,14 +135,7 @@ __global__ void __cluster_dims__(CLC, 1, 1) __launch_bounds__(CLC_NT, 1) k_sa_cl
         p[i] = (uint16_t)a.p[i];
         best_p[i] = (uint16_t)a.best_p[i];
     }
-    if (t == 0) {
-        int e = 0;
-        for (int lx = 0; lx < R; ++lx) {
-            doff[lx] = e;
-            const int x = lx * CLC + c;
-            if (x < n - 1) e += n - 1 - x;
-        }
-    }
+    for (int lx = t; lx < R; lx += CLC_NT) doff[lx] = clc_doff(n, lx * CLC + c);
     __syncthreads();
     for (int i = t; i < R * lda; i += CLC_NT) {
         const int lx = i / lda, y = i - lx * lda, x = lx * CLC + c;
@@ -145,7 +145,9 @@ __global__ void __cluster_dims__(CLC, 1, 1) __launch_bounds__(CLC_NT, 1) k_sa_cl
     }
     for (int lx = warp; lx < R; lx += CLC_NW) {
         const int x = lx * CLC + c;
-        for (int v = x + 1 + lane; v < n; v += 32) Drow[doff[lx] + v - x - 1] = a.D[a.rowaddr[x] + v];
+        const int b = clc_b(x), n4 = clc_n4(n);
+        for (int v = b + lane; v < n4; v += 32)
+            Drow[doff[lx] + v - b] = (v > x && v < n) ? a.D[a.rowaddr[x] + v] : 0;
     }
     ThetaRing<TH_SLOTS> TR = theta_ring<TH_SLOTS>(
         reinterpret_cast<int*>(smem + L.ring), reinterpret_cast<int4*>(smem + L.thdr),
@@ -194,7 +196,7 @@ __global__ void __cluster_dims__(CLC, 1, 1) __launch_bounds__(CLC_NT, 1) k_sa_cl
             const int x = u0 + i_row, lx = x / CLC;
             const int first = i_row == 0 ? v0 : x + 1;
             const int f = i_row == 0 ? 0 : win_f(i_row, L0, m1);    // offset of (x, first)
-            const int32_t* drow = Drow + doff[lx] - x - 1;          // drow[v] = Δ(x, v)
+            const int32_t* drow = Drow + doff[lx] - clc_b(x);       // drow[v] = Δ(x, v)
             for (int v = first + lane; v - lane < n; v += 32) {    // 32 columns at a time, in order
                 const int o = f + v - first;
                 const bool ex = v < n && o < Wl;
@@ -296,7 +298,7 @@ __global__ void __cluster_dims__(CLC, 1, 1) __launch_bounds__(CLC_NT, 1) k_sa_cl
         }
         cl_sync();
         // ---------------- 2. staging vectors, disjoint entries, B' rows ----------------
-        for (int x = t; x < n; x += CLC_NT) {
+        for (int x = t; x < clc_n4(n); x += CLC_NT) {   // (0 past n: the rows are zero-padded)
             dA[x] = (int)ar[x] - (int)as[x];     // a_xr - a_xs (A symmetric)
             dB[x] = (int)br[x] - (int)bs[x];     // B'_xr - B'_xs (PRE-swap, B' symmetric)
         }
@@ -314,10 +316,22 @@ __global__ void __cluster_dims__(CLC, 1, 1) __launch_bounds__(CLC_NT, 1) k_sa_cl
                     brow[r] = brow[s];
                     brow[s] = tr;
                 }
+                // R10 on whole quads of the row: the cells of columns r, s are the touching entries,
+                // overwritten in step 3 after the barrier; padding cells take anything
                 const int dAu = dA[u], dBu = dB[u];
-                int32_t* drow = Drow + doff[lx] - u - 1;
-                for (int v = u + 1 + lane; v < n; v += 32)
-                    if (v != r && v != s) drow[v] += 2 * (dAu - dA[v]) * (dBu - dB[v]);   // R10
+                const int b = clc_b(u), n4 = clc_n4(n);
+                int4* drow4 = reinterpret_cast<int4*>(Drow + doff[lx]);
+                for (int q4 = lane; 4 * q4 < n4 - b; q4 += 32) {
+                    const int v0 = b + 4 * q4;
+                    int4 o = drow4[q4];
+                    const int4 xa = *reinterpret_cast<const int4*>(dA + v0);
+                    const int4 xb = *reinterpret_cast<const int4*>(dB + v0);
+                    o.x += 2 * (dAu - xa.x) * (dBu - xb.x);
+                    o.y += 2 * (dAu - xa.y) * (dBu - xb.y);
+                    o.z += 2 * (dAu - xa.z) * (dBu - xb.z);
+                    o.w += 2 * (dAu - xa.w) * (dBu - xb.w);
+                    drow4[q4] = o;
+                }
             }
         }
         __syncthreads();
@@ -389,11 +403,11 @@ __global__ void __cluster_dims__(CLC, 1, 1) __launch_bounds__(CLC_NT, 1) k_sa_cl
                 const int x = lane == 0 ? r : s;
                 const int val = 2 * (lane == 0 ? sr : ss);
                 const int lo = min(x, v), hi = max(x, v);
-                cl_store(Drow + clc_doff(n, lo) + hi - lo - 1, lo % CLC, val);   // same layout in every CTA
+                cl_store(Drow + clc_doff(n, lo) + hi - clc_b(lo), lo % CLC, val);   // same layout in every CTA
             }
         }
         if (t == 0) {                            // δ''(r, s) = -δ(r, s): swapping back restores the cost
-            cl_store(Drow + clc_doff(n, r) + s - r - 1, r % CLC, -dw);
+            cl_store(Drow + clc_doff(n, r) + s - clc_b(r), r % CLC, -dw);
         }
         // p, the scalars (every CTA keeps them identically), best_p
         __syncthreads();
@@ -426,7 +440,7 @@ __global__ void __cluster_dims__(CLC, 1, 1) __launch_bounds__(CLC_NT, 1) k_sa_cl
     for (int lx = warp; lx < R; lx += CLC_NW) {
         const int x = lx * CLC + c;
         if (x >= n - 1) break;
-        for (int v = x + 1 + lane; v < n; v += 32) a.D[a.rowaddr[x] + v] = Drow[doff[lx] + v - x - 1];
+        for (int v = x + 1 + lane; v < n; v += 32) a.D[a.rowaddr[x] + v] = Drow[doff[lx] + v - clc_b(x)];
     }
     if (c == 0) {
         for (int i = t; i < n; i += CLC_NT) {
