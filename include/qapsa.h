@@ -22,8 +22,12 @@
  *  - Δ layout: upper triangle r < s in row-major enumeration order,
  *    index k(r,s) = r*n - r(r+1)/2 + (s - r - 1)  (R11).  This is also
  *    the candidate order: iteration k proposes the pair with index k mod M.
- *  - All device memory is owned by the context.  Work is issued on the
- *    context's stream; every call returns after that stream is synchronised.
+ *  - All device memory is owned by the context and comes from a per-device
+ *    stream-ordered pool of the library (allocated and released on the
+ *    context's stream, so the stream must outlive the context); released
+ *    buffers are kept for the next context on the device (qap_trim_memory).
+ *    Work is issued on the context's stream; every call returns after that
+ *    stream is synchronised.
  *  - A validation failure returns an error and leaves the context unchanged.
  *    A CUDA failure is sticky: the call returns QAP_E_CUDA and so do all
  *    later calls on that context (qap_last_error() has the CUDA message).
@@ -111,8 +115,16 @@ typedef struct {
 qap_status qap_create(int32_t n, const int32_t* A, const int32_t* B, const int32_t* p0,
                       int32_t device, void* stream, qap_ctx** out);
 
-/* Frees all device memory of ctx (NULL is a no-op). */
+/* Releases all device memory of ctx to the library's device pool (stream-
+ * ordered on the context's stream) and frees ctx (NULL is a no-op). */
 void qap_destroy(qap_ctx* ctx);
+
+/* qap_trim_memory -- returns the unused part of the library's pool on
+ * `device` to the driver (after synchronising the device).  Not on the hot
+ * path: the pool exists so that repeated create / run / destroy cycles (the
+ * end-to-end path) allocate nothing in steady state.
+ * Errors: QAP_E_INVALID_ARG for a bad ordinal, QAP_E_CUDA. */
+qap_status qap_trim_memory(int32_t device);
 
 /* qap_reset -- restart the chain from an assignment: "an initial assignment
  * p" (step (a)) and B' = B[p][p] (R9).  p = perm (n int32 host

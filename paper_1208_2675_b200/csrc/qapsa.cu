@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -24,6 +25,31 @@
 #include "ens_chain.cuh"
 
 using namespace qapsa;
+
+// Device memory: one stream-ordered pool per device, owned by the library.  A freed buffer stays in
+// the pool (release threshold = max) and serves the next context on that device, so the
+// create / run / destroy cycle of the end-to-end path allocates nothing from the driver in steady
+// state (a plain cudaMalloc / cudaFree pair costs milliseconds and, measured on the B200, stalls
+// for up to 100 ms at times).  qap_trim_memory() hands the unused part back.
+static std::mutex g_pool_mu;
+static cudaMemPool_t g_pool[128];
+
+static cudaMemPool_t dev_pool(int dev) {
+    if (dev < 0 || dev >= 128) return nullptr;
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    if (!g_pool[dev]) {
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        cudaMemPool_t pool = nullptr;
+        if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) return nullptr;
+        uint64_t keep = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        g_pool[dev] = pool;
+    }
+    return g_pool[dev];
+}
 
 struct qap_ctx {
     int n = 0, ld = 0, M = 0, dev = 0;
@@ -284,16 +310,41 @@ const char* qap_last_error(const qap_ctx* ctx) {
     return ctx ? ctx->err.c_str() : g_static_err.c_str();
 }
 
+// stream-ordered allocation / release on the context's stream from the device pool
+static cudaError_t dalloc(qap_ctx* c, void* p, size_t bytes) {
+    cudaMemPool_t pool = dev_pool(c->dev);
+    if (!pool) return cudaErrorMemoryAllocation;
+    return cudaMallocFromPoolAsync((void**)p, bytes, pool, c->stream);
+}
+static void dfree(qap_ctx* c, void* p) {
+    if (p) cudaFreeAsync(p, c->stream);
+}
+
+qap_status qap_trim_memory(int32_t device) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
+        return fail(nullptr, QAP_E_INVALID_ARG, "bad device ordinal");
+    cudaMemPool_t pool = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        if (device < 128) pool = g_pool[device];
+    }
+    if (pool && (cudaSetDevice(device) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess ||
+                 cudaMemPoolTrimTo(pool, 0) != cudaSuccess))
+        return fail(nullptr, QAP_E_CUDA, "cudaMemPoolTrimTo failed");
+    return QAP_OK;
+}
+
 void qap_destroy(qap_ctx* c) {
     if (!c) return;
+    cudaSetDevice(c->dev);
     void* ptrs[] = {c->dA, c->dB, c->dp0, c->dp, c->dbest, c->dD, c->dperm, c->dDlin, c->drowaddr,
                     c->dqdesc, c->dst, c->dnear_count,
                     c->dnear_k, c->dnear_dec, c->dscratch, c->ens_p0, c->ens_res, c->ens_best,
                     c->ens_counter, c->dkout, c->dcls, c->dpt, c->dD2, c->tp, c->tbp, c->tD,
                     c->tst, c->tkout, c->ens_near_count, c->ens_near_k, c->ens_near_dec,
                     c->ens_near_chain, c->dtheta, c->dtheta_hdr};
-    for (void* p : ptrs)
-        if (p) cudaFree(p);
+    for (void* p : ptrs) dfree(c, p);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
     if (c->evm) cudaEventDestroy(c->evm);
@@ -372,7 +423,7 @@ qap_status qap_create(int32_t n, const int32_t* A, const int32_t* B, const int32
     qap_status st = QAP_OK;
     auto alloc = [&](void** p, size_t bytes) {
         if (st != QAP_OK) return;
-        if (cudaMalloc(p, bytes) != cudaSuccess) st = fail(nullptr, QAP_E_NOMEM, "cudaMalloc failed");
+        if (dalloc(c, p, bytes) != cudaSuccess) st = fail(nullptr, QAP_E_NOMEM, "device allocation failed");
     };
     alloc(&c->dA, nA);
     alloc(&c->dB, nB);
@@ -579,13 +630,13 @@ qap_status qap_sa_run(qap_ctx* c, uint64_t k0, uint64_t iters, const qap_schedul
     if (tc || clu || rlb) {   // threshold buffer of one chunk of the call (theta_ring.cuh)
         const size_t need = (size_t)((std::min<uint64_t>(iters, TH_CHUNK) + TH_BLK - 1) / TH_BLK) * TH_BLK;
         if (c->theta_cap < need) {
-            if (c->dtheta) cudaFree(c->dtheta);
-            if (c->dtheta_hdr) cudaFree(c->dtheta_hdr);
+            dfree(c, c->dtheta);
+            dfree(c, c->dtheta_hdr);
             c->dtheta = nullptr;
             c->dtheta_hdr = nullptr;
             c->theta_cap = 0;
-            if (cudaMalloc(&c->dtheta, need * 4) != cudaSuccess ||
-                cudaMalloc(&c->dtheta_hdr, need / TH_BLK * sizeof(int4)) != cudaSuccess)
+            if (dalloc(c, &c->dtheta, need * 4) != cudaSuccess ||
+                dalloc(c, &c->dtheta_hdr, need / TH_BLK * sizeof(int4)) != cudaSuccess)
                 return fail(c, QAP_E_NOMEM, "threshold buffer");
             c->theta_cap = need;
         }
@@ -856,26 +907,25 @@ static qap_status ensemble_tc(qap_ctx* c, uint32_t chain_begin, uint32_t chain_c
     const int dstride = c->nqt * 4 + 4;
     CU(cudaSetDevice(c->dev));
     if (c->ens_cap < chain_count) {
-        if (c->ens_p0) cudaFree(c->ens_p0);
-        if (c->ens_res) cudaFree(c->ens_res);
-        if (c->ens_best) cudaFree(c->ens_best);
+        dfree(c, c->ens_p0);
+        dfree(c, c->ens_res);
+        dfree(c, c->ens_best);
         c->ens_p0 = nullptr; c->ens_res = nullptr; c->ens_best = nullptr; c->ens_cap = 0;
-        if (cudaMalloc(&c->ens_p0, (size_t)chain_count * n * 4) != cudaSuccess ||
-            cudaMalloc(&c->ens_res, (size_t)chain_count * sizeof(ChainResult)) != cudaSuccess ||
-            cudaMalloc(&c->ens_best, (size_t)chain_count * n * 2) != cudaSuccess)
+        if (dalloc(c, &c->ens_p0, (size_t)chain_count * n * 4) != cudaSuccess ||
+            dalloc(c, &c->ens_res, (size_t)chain_count * sizeof(ChainResult)) != cudaSuccess ||
+            dalloc(c, &c->ens_best, (size_t)chain_count * n * 2) != cudaSuccess)
             return fail(c, QAP_E_NOMEM, "ensemble buffers");
         c->ens_cap = chain_count;
     }
     if (c->tcap < chain_count) {
         void* ptrs[] = {c->tp, c->tbp, c->tD, c->tst, c->tkout};
-        for (void* q : ptrs)
-            if (q) cudaFree(q);
+        for (void* q : ptrs) dfree(c, q);
         c->tp = c->tbp = c->tD = nullptr; c->tst = nullptr; c->tkout = nullptr; c->tcap = 0;
-        if (cudaMalloc(&c->tp, (size_t)chain_count * n * 4) != cudaSuccess ||
-            cudaMalloc(&c->tbp, (size_t)chain_count * n * 4) != cudaSuccess ||
-            cudaMalloc(&c->tD, (size_t)chain_count * dstride * 4) != cudaSuccess ||
-            cudaMalloc(&c->tst, (size_t)chain_count * sizeof(DevState)) != cudaSuccess ||
-            cudaMalloc(&c->tkout, (size_t)chain_count * 2 * sizeof(unsigned long long)) != cudaSuccess)
+        if (dalloc(c, &c->tp, (size_t)chain_count * n * 4) != cudaSuccess ||
+            dalloc(c, &c->tbp, (size_t)chain_count * n * 4) != cudaSuccess ||
+            dalloc(c, &c->tD, (size_t)chain_count * dstride * 4) != cudaSuccess ||
+            dalloc(c, &c->tst, (size_t)chain_count * sizeof(DevState)) != cudaSuccess ||
+            dalloc(c, &c->tkout, (size_t)chain_count * 2 * sizeof(unsigned long long)) != cudaSuccess)
             return fail(c, QAP_E_NOMEM, "tensor-memory ensemble buffers");
         c->tcap = chain_count;
     }
@@ -995,17 +1045,17 @@ qap_status qap_ensemble_run(qap_ctx* c, uint32_t chain_begin, uint32_t chain_cou
     const int smem = a_bytes + groups * L.bytes;
     CU(cudaSetDevice(c->dev));
     if (c->ens_cap < chain_count) {
-        if (c->ens_p0) cudaFree(c->ens_p0);
-        if (c->ens_res) cudaFree(c->ens_res);
-        if (c->ens_best) cudaFree(c->ens_best);
+        dfree(c, c->ens_p0);
+        dfree(c, c->ens_res);
+        dfree(c, c->ens_best);
         c->ens_p0 = nullptr; c->ens_res = nullptr; c->ens_best = nullptr; c->ens_cap = 0;
-        if (cudaMalloc(&c->ens_p0, (size_t)chain_count * n * 4) != cudaSuccess ||
-            cudaMalloc(&c->ens_res, (size_t)chain_count * sizeof(ChainResult)) != cudaSuccess ||
-            cudaMalloc(&c->ens_best, (size_t)chain_count * n * 2) != cudaSuccess)
+        if (dalloc(c, &c->ens_p0, (size_t)chain_count * n * 4) != cudaSuccess ||
+            dalloc(c, &c->ens_res, (size_t)chain_count * sizeof(ChainResult)) != cudaSuccess ||
+            dalloc(c, &c->ens_best, (size_t)chain_count * n * 2) != cudaSuccess)
             return fail(c, QAP_E_NOMEM, "ensemble buffers");
         c->ens_cap = chain_count;
     }
-    if (!c->ens_counter) CU(cudaMalloc(&c->ens_counter, sizeof(unsigned int)));
+    if (!c->ens_counter) CU(dalloc(c, &c->ens_counter, sizeof(unsigned int)));
     if (p0s) CU(cudaMemcpyAsync(c->ens_p0, p0s, (size_t)chain_count * n * 4, cudaMemcpyHostToDevice, c->stream));
     CU(cudaMemsetAsync(c->ens_counter, 0, sizeof(unsigned int), c->stream));
     CU(cudaMemsetAsync(c->ens_near_count, 0, sizeof(unsigned int), c->stream));
@@ -1077,11 +1127,11 @@ qap_status qap_start_perms(qap_ctx* c, uint64_t seed, uint32_t chain_begin, uint
     if (!out || count == 0) return fail(c, QAP_E_INVALID_ARG, "out is NULL or count is 0");
     CU(cudaSetDevice(c->dev));
     int32_t* d = nullptr;
-    CU(cudaMallocAsync(&d, (size_t)count * c->n * 4, c->stream));
+    CU(dalloc(c, &d, (size_t)count * c->n * 4));
     k_start_perms<<<(count + 127) / 128, 128, 0, c->stream>>>(c->n, seed, chain_begin, (int)count, d);
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaMemcpyAsync(out, d, (size_t)count * c->n * 4, cudaMemcpyDeviceToHost, c->stream);
-    cudaFreeAsync(d, c->stream);
+    dfree(c, d);
     CU(e);
     CU(cudaStreamSynchronize(c->stream));
     c->last_launches = 1;

@@ -35,7 +35,7 @@ QAP_NEAR_LOG_CAP = 1024
 QAP_ENS_NEAR_LOG_CAP = 65536
 
 # Every symbol include/qapsa.h declares (checked by tests/test_abi.py).
-EXPORTS = ("qap_create", "qap_destroy", "qap_reset", "qap_delta_init", "qap_sa_run", "qap_cost",
+EXPORTS = ("qap_create", "qap_destroy", "qap_trim_memory", "qap_reset", "qap_delta_init", "qap_sa_run", "qap_cost",
            "qap_get_state", "qap_get_near_ties", "qap_schedule_bounds", "qap_ensemble_run",
            "qap_ensemble_near_ties", "qap_start_perms",
            "qap_set_option", "qap_uses_tensor_core", "qap_engine", "qap_last_kernel_time", "qap_last_scratch_time",
@@ -85,6 +85,7 @@ def lib(build_if_missing: bool = True):
     L.qap_create.argtypes = [C.c_int32, i32p, i32p, i32p, C.c_int32, vp, C.POINTER(vp)]
     L.qap_destroy.argtypes = [vp]
     L.qap_destroy.restype = None
+    L.qap_trim_memory.argtypes = [C.c_int32]
     L.qap_reset.argtypes = [vp, i32p]
     L.qap_delta_init.argtypes = [vp]
     L.qap_sa_run.argtypes = [vp, C.c_uint64, C.c_uint64, C.POINTER(qap_schedule), C.c_uint64,
@@ -163,6 +164,11 @@ def qap_create(A, B, p0, device: int = 0, stream=None):
 
 def qap_destroy(ctx):
     lib().qap_destroy(ctx)
+
+
+def qap_trim_memory(device=0):
+    """Return the unused part of the library's device pool on `device` to the driver."""
+    _check(lib().qap_trim_memory(device))
 
 
 def qap_reset(ctx, perm=None):

@@ -813,3 +813,35 @@ def test_switch_gap_invariance(gap):
     I = 150000
     sch = O.geometric_schedule_for(A, B, p0, I)
     _compare_run(A, B, p0, I, sch, opts=[(Q.QAP_OPT_SWITCH_GAP, gap)], k_splits=[0, 50001, I])
+
+
+def test_device_pool_reuse_across_contexts_and_streams():
+    """Device buffers come from the library's stream-ordered pool (qapsa.cu dev_pool): contexts
+    created, run and destroyed back to back on two streams, with a larger context (N = 256,
+    relabel engine, bigger buffers) in between, reuse released buffers and every run still
+    reproduces the oracle's trajectory; qap_trim_memory hands the pool back."""
+    A, B, p0, cfg = config(1)
+    I = cfg["iters"]
+    sch = O.geometric_schedule_for(A, B, p0, I)
+    o = None
+    Ab, Bb = grey_density(256)
+    pb = start_perm(256, 5, 0)
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    for rep in range(6):
+        st = streams[rep % 2]
+        with Q.Solver(A, B, p0, stream=st.cuda_stream) as s:
+            s.delta_init()
+            g = s.run(0, I, _sched(sch), SA_SEED)
+            n_near, near = s.near_ties()
+            if o is None:
+                o = O.Run(A, B, p0).run(0, I, sch, SA_SEED, follow=near)
+            assert (g["cost"], g["best_cost"], g["accepted"], g["digest"]) == (
+                o["cost"], o["best_cost"], o["accepted"], o["digest"]), rep
+        if rep == 2:
+            with Q.Solver(Ab, Bb, pb, stream=st.cuda_stream) as s:
+                s.delta_init()
+                s.run(0, 20000, _sched(O.geometric_schedule_for(Ab, Bb, pb, 20000)), SA_SEED)
+                assert s.cost() == O.cost(Ab, Bb, s.state()[0])
+    Q.qap_trim_memory(0)
+    with pytest.raises(Q.QapError):
+        Q.qap_trim_memory(-1)
