@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
                 // exact integer threshold (R23); δ <= 0 accepted (R5); a flagged iteration takes
                 // the general test (float θ with a margin, exact inside it, near ties flagged)
                 const int thr = TR.at_ofs((int)(k - TR.kb) + t);
-                if (d <= thr || d <= 0) {
+                if (d <= max(thr, 0)) {                   // (thr = -1 when flagged)
                     acc = true;
                 } else if (thr < 0 && (float)d <= rejT) {  // else certain reject (chain.cuh)
                     acc = metropolis_fast(d, a.sch, k + (uint64_t)t, a.seed, 0u, &near);

@@ -75,7 +75,10 @@ __host__ __device__ inline ScLayout sc_layout(int ld) {
 // Window geometry of this row warp (rows h2, h2 + 1 of the window at cursor (u0, v0), at most W
 // candidates and rem iterations): rf = first column of the row (n if the row is not in the window),
 // rb = offset base (candidate (u0 + i, v) has offset rb + v), Wl = candidates in the window.
-struct ScWin { int Wl; int rb[2]; int rf[2]; };
+// Window geometry of this warp's rows i = h2 + e: row i's candidates are the locations
+// v in [rf, n) at offsets o = rb + v; v takes part iff 0 <= v - rf < lim (lim = the row's
+// candidates inside the window, 0 for rows past the window), one unsigned compare.
+struct ScWin { int Wl; int rb[2]; int rf[2]; int lim[2]; };
 __device__ __forceinline__ ScWin sc_win(int n, int u0, int v0, int W, uint32_t rem, int h2) {
     const int R = win_rows<4>(n, u0), L0 = n - v0, m1 = n - 1 - u0;
     ScWin w;
@@ -84,8 +87,10 @@ __device__ __forceinline__ ScWin sc_win(int n, int u0, int v0, int W, uint32_t r
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
         const int i = h2 + e;
+        const int f = i == 0 ? 0 : win_f(i, L0, m1);
         w.rf[e] = i >= R ? n : i == 0 ? v0 : u0 + i + 1;
-        w.rb[e] = (i == 0 ? 0 : win_f(i, L0, m1)) - w.rf[e];
+        w.rb[e] = f - w.rf[e];
+        w.lim[e] = i >= R ? 0 : max(0, min(w.Wl - f, n - w.rf[e]));
     }
     return w;
 }
@@ -292,13 +297,15 @@ __global__ void __launch_bounds__(tcs_nt<ENS>(), ENS ? 2 : 1) k_sa_scratch(const
             const int auv = As[u * ld + v], buv = Bs[pu[e] * ld + px];
             dd[e] = 2 * (guv + (int)gv[e] - Dg[u] - dv + 2 * auv * buv);   // δ(u, v) (R10d)
             const int o = wg.rb[e] + v;
-            const bool ex = vin && v >= wg.rf[e] && o < Wl;     // (rows i >= R have rf = n)
+            const bool ex = (unsigned)(v - wg.rf[e]) < (unsigned)wg.lim[e];
             if (RING) {
-                // exact integer threshold (R23): accept iff δ <= thr; a flagged iteration (thr < 0)
-                // takes the general test below
+                // exact integer threshold (R23): accept iff δ <= thr; a flagged iteration (thr = -1)
+                // accepts δ <= 0 (R5) and takes the general test below for δ > 0: both are
+                // δ <= max(thr, 0)
                 const int thr = TR.at_ofs(kofs0 + (int)kr + o);
-                acc_mask |= (unsigned)(ex && (dd[e] <= thr || (thr < 0 && dd[e] <= 0))) << e;   // (R5)
-                need |= (unsigned)(ex && thr < 0 && dd[e] > 0) << e;
+                const bool pass = dd[e] <= max(thr, 0);
+                acc_mask |= (unsigned)(ex && pass) << e;
+                need |= (unsigned)(ex && !pass && thr < 0) << e;
             } else {
                 // ensemble: θ_k -+ its margin from the producer's ring (prepare_theta), decided
                 // outside the bracket, exact double test inside it (R16); δ <= 0 accepted (R5)

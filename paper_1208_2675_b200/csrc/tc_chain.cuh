@@ -444,8 +444,9 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
                             if (u0 + i0 + i < v) dd[i] = (uint32_t)row[u0 + i0 + i];
                     }
                     int mn = INT_MAX;                // smallest δ of the thread's candidates
+                    // (lo <= 1, and lo > 0 only in the first group: the lower bound binds at i = 0 alone)
     #pragma unroll
-                    for (int i = 0; i < 8; ++i) mn = min(mn, (i >= lo && i <= hi) ? (int)dd[i] : INT_MAX);
+                    for (int i = 0; i < 8; ++i) mn = min(mn, ((i > 0 || lo <= 0) && i <= hi) ? (int)dd[i] : INT_MAX);
                     unsigned am = 0;
                     int oo[8];
                     if (__any_sync(0xffffffffu, mn <= sp.y)) {   // else every candidate is above every threshold
@@ -456,7 +457,7 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
                             oo[i] = f - first + v;
                             f += ii == 0 ? L0 : m1 - ii;
                             const int thr = TR.ring[(kofs + oo[i]) & (TR.RING - 1)];
-                            am |= (unsigned)(i >= lo && i <= hi && (int)dd[i] <= thr) << i;
+                            am |= (unsigned)((i > 0 || lo <= 0) && i <= hi && (int)dd[i] <= thr) << i;
                         }
                     }
                     if (__any_sync(0xffffffffu, am != 0)) {
