@@ -52,7 +52,7 @@ __host__ __device__ inline E4Layout e4_layout(int n, int ld) {
     L.dg = o;    o += 128 * 4;                       // D_x = G[x][p(x)]
     L.grow = o;  o += 4 * 128 * 4;                   // the window's rows of G: G[u_i][f]
     L.slots = o; o += 2 * 4 * 16;
-    L.ering = o; o += E4_ERING * 8;                  // (θ - m, θ + m) ring of the producer warp
+    L.ering = o; o += E4_ERING * 8;                  // integer (θ - m, θ + m) ring of the producer warp (int_bracket)
     L.ebar = o;  o += 2 * (E4_ERING / E4_EB) * 8;    // full[NB], empty[NB]
     L.ectl = o;  o += 16;                            // stop flag
     L.misc = o;  o += 16;                            // mbarrier | TMEM base
@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(E4_NT, 4) k_ens_scratch(const ChainArgs a, uns
     int* Dg = reinterpret_cast<int*>(smem + L.dg);
     int* grow = reinterpret_cast<int*>(smem + L.grow);
     int4* slots = reinterpret_cast<int4*>(smem + L.slots);
-    float2* ering = reinterpret_cast<float2*>(smem + L.ering);
+    int2* ering = reinterpret_cast<int2*>(smem + L.ering);
     uint64_t* ebar = reinterpret_cast<uint64_t*>(smem + L.ebar);
     volatile int* ectl = reinterpret_cast<volatile int*>(smem + L.ectl);
     uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + L.misc);
@@ -208,13 +208,14 @@ __global__ void __launch_bounds__(E4_NT, 4) k_ens_scratch(const ChainArgs a, uns
             tc::tmem_wait_ld();
         }
         group_sync(3, 128);                      // the window's rows of G exchanged
-        int rb[4], rf[4];
+        int rb[4], rf[4], lim[4];                // row i: locations [rf, n) at offsets rb + v, lim of them in the window
         {
             int f = 0;
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 rf[i] = i >= R ? n : i == 0 ? v0 : u0 + i + 1;
                 rb[i] = f - rf[i];
+                lim[i] = i >= R ? 0 : max(0, min(Wl - f, n - rf[i]));
                 f += i == 0 ? L0 : m1 - i;
             }
         }
@@ -229,12 +230,12 @@ __global__ void __launch_bounds__(E4_NT, 4) k_ens_scratch(const ChainArgs a, uns
             const int auv = As[u * ld + v], buv = Bs[pu[i] * ld + px];
             dd[i] = 2 * (guv + (int)gv[i] - Dg[u] - dv + 2 * auv * buv);   // δ(u, v) (R10d)
             const int o = rb[i] + v;
-            const bool ex = vin && v >= rf[i] && o < Wl;
-            // θ_k -+ its margin from the producer (prepare_theta); δ <= 0 accepted (R5)
-            const float2 th = ering[((int)kr + o) & (E4_ERING - 1)];
-            const float df = (float)dd[i];
-            acc_mask |= (unsigned)(ex && (dd[i] <= 0 || df < th.x)) << i;
-            band |= (unsigned)(ex && dd[i] > 0 && !(df < th.x) && !(df > th.y)) << i;
+            const bool ex = (unsigned)(v - rf[i]) < (unsigned)lim[i];
+            // θ_k -+ its margin from the producer as integers (int_bracket); δ <= 0 accepted (R5)
+            const int2 th = ering[((int)kr + o) & (E4_ERING - 1)];
+            const int lo = max(th.x, 0);
+            acc_mask |= (unsigned)(ex & (dd[i] <= lo)) << i;
+            band |= (unsigned)(ex & (dd[i] > lo) & (dd[i] <= th.y)) << i;
         }
         if (__any_sync(0xffffffffu, band != 0)) {
 #pragma unroll
@@ -363,7 +364,7 @@ __global__ void __launch_bounds__(E4_NT, 4) k_ens_scratch(const ChainArgs a, uns
             Prep pr;
             pr.k = k0 + (uint64_t)b * E4_EB + (uint64_t)i;
             prepare_theta(pr, sch, seed, cv.chain);
-            ering[(b * E4_EB + i) & (E4_ERING - 1)] = make_float2(pr.th - pr.m, pr.th + pr.m);
+            ering[(b * E4_EB + i) & (E4_ERING - 1)] = int_bracket(pr.th, pr.m);
         }
         __syncwarp();
         if (lane == 0) {

@@ -65,7 +65,7 @@ __host__ __device__ inline ScLayout sc_layout(int ld) {
     L.misc = o;  o += 64;                       // mbarrier | TMEM base
     L.tbar = o;  o += TH_SLOTS * 8;             // threshold ring mbarriers
     L.thdr = o;  o += TH_SLOTS * 16;            // threshold ring block headers
-    L.ering = o; o += TCS_ERING * 8;            // ensemble: (θ - m, θ + m) ring (float2) of the producer warp
+    L.ering = o; o += TCS_ERING * 8;            // ensemble: integer (θ - m, θ + m) ring of the producer warp (int_bracket)
     L.ebar = o;  o += (TCS_ERING / TCS_EB) * 16; //   its block mbarriers: full[NB], empty[NB]
     L.ectl = o;  o += 16;                       //   stop flag
     L.bytes = o;
@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(tcs_nt<ENS>(), ENS ? 2 : 1) k_sa_scratch(const
     int4* slots = reinterpret_cast<int4*>(smem + L.slots);
     int* rec = reinterpret_cast<int*>(smem + L.rec);
     uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + L.misc);          // G|H update done
-    float2* ering = reinterpret_cast<float2*>(smem + L.ering);            // ensemble θ bracket ring
+    int2* ering = reinterpret_cast<int2*>(smem + L.ering);                // ensemble θ bracket ring
     uint64_t* ebar = reinterpret_cast<uint64_t*>(smem + L.ebar);          // [0, NB) full, [NB, 2NB) empty
     volatile int* ectl = reinterpret_cast<volatile int*>(smem + L.ectl);  // [1] stop
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.misc + 8);
@@ -309,10 +309,10 @@ __global__ void __launch_bounds__(tcs_nt<ENS>(), ENS ? 2 : 1) k_sa_scratch(const
             } else {
                 // ensemble: θ_k -+ its margin from the producer's ring (prepare_theta), decided
                 // outside the bracket, exact double test inside it (R16); δ <= 0 accepted (R5)
-                const float2 th = ering[((int)kr + o) & (TCS_ERING - 1)];
-                const float df = (float)dd[e];
-                acc_mask |= (unsigned)(ex && (dd[e] <= 0 || df < th.x)) << e;
-                band |= (unsigned)(ex && dd[e] > 0 && !(df < th.x) && !(df > th.y)) << e;
+                const int2 th = ering[((int)kr + o) & (TCS_ERING - 1)];
+                const int lo = max(th.x, 0);
+                acc_mask |= (unsigned)(ex & (dd[e] <= lo)) << e;
+                band |= (unsigned)(ex & (dd[e] > lo) & (dd[e] <= th.y)) << e;
             }
         }
         if (__any_sync(0xffffffffu, (need | band) != 0)) {   // general test: float θ, exact inside its margin
@@ -507,7 +507,7 @@ __global__ void __launch_bounds__(tcs_nt<ENS>(), ENS ? 2 : 1) k_sa_scratch(const
             Prep pr;
             pr.k = k0 + (uint64_t)b * TCS_EB + (uint64_t)i;
             prepare_theta(pr, sch, seed, cv.chain);
-            ering[(b * TCS_EB + i) & (TCS_ERING - 1)] = make_float2(pr.th - pr.m, pr.th + pr.m);
+            ering[(b * TCS_EB + i) & (TCS_ERING - 1)] = int_bracket(pr.th, pr.m);
         }
         __syncwarp();
         if (lane == 0) {

@@ -182,6 +182,13 @@ __device__ __forceinline__ void theta_of(const Sched& sch, uint64_t seed, uint32
     *th = pr.th;
     *m = pr.m;
 }
+// The float bracket (θ - m, θ + m) as integers for δ: accepted outright iff δ <= max(lo, 0)
+// (δ < θ - m, or δ <= 0 by R5), rejected outright iff δ > hi (δ > θ + m), the exact test in
+// between.  Exact for |δ| < 2^24, where (float)δ is exact (tensor-memory instances: |δ| <=
+// 4 n 127^2 < 2^24); brackets past 2^30 are clamped (every such δ is on the same side).
+__device__ __forceinline__ int2 int_bracket(float th, float m) {
+    return make_int2((int)ceilf(fminf(th - m, 1073741824.0f)) - 1, (int)floorf(fminf(th + m, 1073741824.0f)));
+}
 // exact double-precision Eq.(2) inside the float margin (rare; kept out of line):
 // bit 0 = accept, bit 1 = near tie (R16)
 __device__ __noinline__ int tc_exact(int d, uint64_t kk, Sched sch, uint64_t seed, uint32_t chain) {
