@@ -478,19 +478,30 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
                         break;
                     }
                 }
-            } else
+            } else {
+            // the thread's candidate rows as in the fast path (a superset where the window is cut
+            // short): a group whose candidates all lie above rejI holds no accept (prefilter)
+            const int ulo = v >= v0 ? u0 : u0 + 1;
+            const int uhi = vin ? min(v - 1, u0 + R - 1) : -1;
             for (int g = warp >> 2; g < NG; g += 2) {
                 const int i0 = 8 * g;
                 int f = i0 == 0 ? 0 : win_f(i0, L0, m1);   // offset of row u0 + i0's first candidate
                 if (f >= Wl) break;                  // warp-uniform: the group starts past the window
                 uint32_t dd[8];
                 tc::tmem_ld8(tm + quad_lane + (uint32_t)(u0 + i0), dd);   // columns u0+i0 .. (< 140: inside G, unused)
+                const int lo = ulo - u0 - i0, hi = uhi - u0 - i0;
                 tc::tmem_wait_ld();
                 if (v == pend_r || v == pend_s) {    // cells still being patched: their new values
                     const int* row = v == pend_r ? rowR : rowS;
     #pragma unroll
                     for (int i = 0; i < 8; ++i)
                         if (u0 + i0 + i < v) dd[i] = (uint32_t)row[u0 + i0 + i];
+                }
+                {
+                    int mn = INT_MAX;
+    #pragma unroll
+                    for (int i = 0; i < 8; ++i) mn = min(mn, ((i > 0 || lo <= 0) && i <= hi) ? (int)dd[i] : INT_MAX);
+                    if (!__any_sync(0xffffffffu, mn <= rejI)) continue;   // every candidate a certain reject
                 }
                 // per candidate: exists / accepted outright (δ <= 0, R5) / needs the threshold test
                 unsigned need = 0, am = 0;
@@ -541,6 +552,7 @@ __global__ void __launch_bounds__(TCK_NT, 1) k_sa_tc(const ChainArgs a) {
                     }
                     break;
                 }
+            }
             }
         }
         {
