@@ -201,11 +201,13 @@ __global__ void __cluster_dims__(CLC, 1, 1) __launch_bounds__(CLC_NT, 1) k_sa_cl
                 const int o = f + v - first;
                 const bool ex = v < n && o < Wl;
                 const int d = ex ? drow[v] : 0;
-                bool acc = false;
-                if (ex) {
-                    const int thr = TR.at_ofs(ko + o);
-                    acc = d <= thr || (thr < 0 && d <= 0);          // R23; δ <= 0 accepted (R5)
-                    if (thr < 0 && d > 0) {      // flagged iteration: general test (R16)
+                const int thr = ex ? TR.at_ofs(ko + o) : 0;
+                // R23; δ <= 0 accepted (R5); a flagged iteration (thr = -1) with δ > 0 takes the
+                // general test (branch-free in the common case: a warp vote guards the rare one)
+                bool acc = ex & (d <= max(thr, 0));
+                const bool need = ex & (thr < 0) & (d > 0);
+                if (__any_sync(0xffffffffu, need)) {
+                    if (need) {                  // flagged iteration: general test (R16)
                         float th, m;
                         theta_of(sch, seed, 0u, k0 + kr + (uint64_t)o, &th, &m);
                         const float df = (float)d;

@@ -223,13 +223,8 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
     __syncthreads();
     if (CL > 1) { cl_arrive(); cl_wait(); }               // every CTA's share loaded
 
-    // Δ~ entry e (int index of the quad layout): read (any CTA's share), write (owner only)
-    auto drd = [&](int e) -> int {
-        if (CL == 1) return D[e];
-        const int g = e >> 2, own = g % CL;
-        const int32_t* loc = Ds + 4 * (g / CL) + (e & 3);
-        return own == crank ? *loc : cl_load(loc, own);
-    };
+    // Δ~ entry e (int index of the quad layout; quad g lives in CTA g mod CL at slot g / CL):
+    // write (owner only)
     auto dwr = [&](int e, int v) {                        // replicated value: owner stores
         if (CL == 1) { D[e] = v; return; }
         const int g = e >> 2;
@@ -305,29 +300,33 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
         if (CL > 1 && pend_wait) { cl_wait(); pend_wait = false; }   // other CTAs' updates visible
         // ---- window: candidates (r, s0 + t), t < Wl
         const int cr = ncls ? cls[r] : 0xFF;
-        bool acc = false, near = false, twin = false;
-        int d = 0, sab = 0, s = s0 + t;
-        uint16_t newsig = 0;
-        if (t < Wl) {
-            const int pv = cr != 0xFF ? pt[cr * (n + 1) + s] : 0xFFFF;
-            const int sr = (pv != 0xFFFF && pv >= s0) ? sig[pv] : sig[r];   // σ(r) at this candidate
-            twin = cr != 0xFF && cls[s] == cr;
-            if (twin) {
-                newsig = (uint16_t)sr;                    // σ(s) after the transposition (r s)
-            } else {
-                const int ss = sig[s];
-                const int sa = min(sr, ss), sb = max(sr, ss);
-                sab = (sa << 16) | sb;
-                d = drd(rowaddr[sa] + sb);
-                // exact integer threshold (R23); δ <= 0 accepted (R5); a flagged iteration takes
-                // the general test (float θ with a margin, exact inside it, near ties flagged)
-                const int thr = TR.at_ofs((int)(k - TR.kb) + t);
-                if (d <= max(thr, 0)) {                   // (thr = -1 when flagged)
-                    acc = true;
-                } else if (thr < 0 && (float)d <= rejT) {  // else certain reject (chain.cuh)
-                    acc = metropolis_fast(d, a.sch, k + (uint64_t)t, a.seed, 0u, &near);
-                }
-            }
+        // (branch-free: every lane loads; a lane past the window reads location r + 1 <= n - 1)
+        bool near = false;
+        const int s = s0 + t;
+        const bool live = t < Wl;
+        const int sc = live ? s : r + 1;
+        const int pv = cr != 0xFF ? pt[cr * (n + 1) + sc] : 0xFFFF;
+        const int sr = (pv != 0xFFFF && pv >= s0) ? sig[pv] : sig[r];   // σ(r) at this candidate
+        const bool twin = live & (cr != 0xFF) & (cls[sc] == cr);
+        const uint16_t newsig = (uint16_t)sr;             // σ(s) after the transposition (r s), if twin
+        const int ss = sig[sc];
+        const int ca = min(sr, ss), cb = max(sr, ss);   // the candidate's slot pair
+        const int sab = (ca << 16) | cb;
+        const bool cross = live & !twin;
+        int d = 0;
+        if (cross) {                                      // Δ~(sa, sb) from its owner CTA
+            const int e = rowaddr[ca] + cb;
+            if (CL == 1) d = D[e];
+            else d = cl_load(Ds + 4 * ((e >> 2) / CL) + (e & 3), (e >> 2) % CL);
+        }
+        // exact integer threshold (R23); δ <= 0 accepted (R5); a flagged iteration (thr = -1)
+        // with δ > 0 takes the general test (float θ with a margin, exact inside it, near ties
+        // flagged) unless δ is a certain reject (chain.cuh)
+        const int thr = TR.at_ofs((int)(k - TR.kb) + t);
+        bool acc = cross & (d <= max(thr, 0));
+        const bool need = cross & (thr < 0) & (d > 0) & ((float)d <= rejT);
+        if (__any_sync(0xffffffffu, need)) {
+            if (need) acc = metropolis_fast(d, a.sch, k + (uint64_t)t, a.seed, 0u, &near);
         }
         int4* slots = slot_base + parity * RLB_NW;
         unsigned* twm = twm_base + parity * RLB_NW;
