@@ -234,12 +234,16 @@ __global__ void __launch_bounds__(tcs_nt<ENS>(), ENS ? 2 : 1) k_sa_scratch(const
     int ring_blo = -1, ring_hi = 0;              // ring: last block refilled from, offsets known resident
     int ering_ready = 0, ering_freed = 0;        // ensemble: producer blocks known complete / released
     static_assert(TH_BLK == 1024, "ring_blo counts 1024-iteration blocks");
-    while (kr < kr_end && kr - kr_last < gap) {
+    while ((kr < kr_end) & (kr - kr_last < gap)) {
         // ---------------- window: rows u0 .. u0+R-1 (R <= 4) ----------------
         TCT_MARK(pt0, u0 + v0);
         const int Wl = wg.Wl;
+        // the loop top's rare cases behind one uniform branch: a threshold block passed or not yet
+        // known resident, or the window's rows to be read afresh
+        const int ko = kofs0 + (int)kr;
+        const bool slow = RING ? (((ko >> 10) != ring_blo) | (ko + Wl > ring_hi) | fresh) : true;
+      if (slow) {
         if (RING) {
-            const int ko = kofs0 + (int)kr;
             if ((ko >> 10) != ring_blo) {     // a block passed: its slot can be refilled (uniform test)
                 ring_blo = ko >> 10;
                 if (t == 0) TR.refill(k0 + kr);
@@ -283,6 +287,7 @@ __global__ void __launch_bounds__(tcs_nt<ENS>(), ENS ? 2 : 1) k_sa_scratch(const
             }
             group_sync(3, 32 * TCS_RW);          // exchange
         }
+      }
         TCT_ACC(0, pt0, xch[v]);
         int4* sl = slots + parity * TCS_RW;
         unsigned acc_mask = 0, near_mask = 0;
@@ -382,8 +387,10 @@ __global__ void __launch_bounds__(tcs_nt<ENS>(), ENS ? 2 : 1) k_sa_scratch(const
         const uint32_t kracc = kr + (uint32_t)j;
         TCT_ACC(5, pt1, r + ps);
         // ---------------- stage: the G|H update operands, D'', the next window's rows ----------------
-        int nu0, nv0;                            // next window: cursor after (r, s)
-        next_pair(n, r, s, &nu0, &nv0);
+        // next window: cursor after (r, s) (next_pair as selects)
+        const bool same_row = s + 1 < n, next_row = r + 1 < n - 1;
+        const int nu0 = same_row ? r : next_row ? r + 1 : 0;
+        const int nv0 = same_row ? s + 1 : next_row ? r + 2 : 1;
         int npu[2], nu[2];                       // this warp's next rows and their facilities after the swap
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
