@@ -409,12 +409,10 @@ __global__ void __launch_bounds__(tcs_nt<ENS>(), ENS ? 2 : 1) k_sa_scratch(const
             dAu[e] = (int)As[nu[e] * ld + r] - (int)As[nu[e] * ld + s];
             dBfu[e] = (int)Bs[npu[e] * ld + pr] - (int)Bs[npu[e] * ld + ps];
         }
-        int dB = 0, ars = 0, brs = 0;
-        if (h2 == 0) {                           // D'' below (one thread per v)
-            dB = vin ? (int)Bs[pr * ld + px] - (int)Bs[ps * ld + px] : 0;
-            ars = As[r * ld + s];
-            brs = Bs[pr * ld + ps];
-        }
+        // D'' below (stored by the h2 = 0 warps; loaded by all: no branch)
+        // (v >= n reads padding or the next row: in bounds, never used)
+        const int dB = (int)Bs[pr * ld + px] - (int)Bs[ps * ld + px];
+        const int ars = As[r * ld + s], brs = Bs[pr * ld + ps];
         if (mma_pending) {                       // the previous update complete: tensor memory is current
             if (!mma_done) tc::mbar_wait(mbar, ph);
             ph ^= 1;
@@ -427,13 +425,10 @@ __global__ void __launch_bounds__(tcs_nt<ENS>(), ENS ? 2 : 1) k_sa_scratch(const
             tc::tmem_ld1(tm + quad_lane + TCS_COL_G + (uint32_t)npu[e], g4[e]);
             tc::tmem_ld1(tm + quad_lane + TCS_COL_H + (uint32_t)nu[e], h4[e]);
         }
-        // G[v][p(s)], G[v][p(r)]: needed by lanes r and s only (their new diagonal), so only the
-        // h2 = 0 warps of those lanes' quadrants load them (warp-uniform)
-        const int q4 = warp & 3;
-        if (h2 == 0 && ((r >> 5) == q4 || (s >> 5) == q4)) {
-            tc::tmem_ld1(tm + quad_lane + TCS_COL_G + (uint32_t)ps, gps);
-            tc::tmem_ld1(tm + quad_lane + TCS_COL_G + (uint32_t)pr, gpr);
-        }
+        // G[v][p(s)], G[v][p(r)]: needed by lanes r and s only (their new diagonal); loaded by
+        // every warp (no branch)
+        tc::tmem_ld1(tm + quad_lane + TCS_COL_G + (uint32_t)ps, gps);
+        tc::tmem_ld1(tm + quad_lane + TCS_COL_G + (uint32_t)pr, gpr);
         const int dA = vin ? arv - asv : 0, dBf = vin ? bfr - bfs : 0;
         if (h2 != 0) {                           // the update's operands (one thread per v, the h2 = 1 warps)
             const int ro = (v >> 3) * 256 + (v & 7) * 16;
@@ -452,11 +447,11 @@ __global__ void __launch_bounds__(tcs_nt<ENS>(), ENS ? 2 : 1) k_sa_scratch(const
         }
         TCT_ACC(9, pt1, dAu[1] + dBfu[1] + arv + bfs);
         tc::tmem_wait_ld();
-        if (h2 == 0) {                           // D'' (one thread per v)
-            const int dnew = (v == r) ? (int)gps + ars * brs : (v == s) ? (int)gpr + ars * brs : dv - dA * dB;
-            if (vin) Dg[v] = dnew;
-            if (v == r) p[v] = (uint16_t)ps;
-            if (v == s) p[v] = (uint16_t)pr;
+        {                                        // D'' (one thread per v: the h2 = 0 warps store)
+            const int dnew = ((v == r) | (v == s)) ? (int)(v == r ? gps : gpr) + ars * brs : dv - (vin ? dA * dB : 0);
+            const bool own = (h2 == 0) & vin;
+            if (own) Dg[v] = dnew;
+            if (own & ((v == r) | (v == s))) p[v] = (uint16_t)(v == r ? ps : pr);
         }
         TCT_ACC(8, pt1, (int)(h4[1] + g4[1]));
         px = (v == r) ? ps : (v == s) ? pr : px;     // p(v), p^-1(v) after the swap
