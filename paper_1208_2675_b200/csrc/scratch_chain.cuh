@@ -297,7 +297,7 @@ __global__ void __launch_bounds__(tcs_nt<ENS>(), ENS ? 2 : 1) k_sa_scratch(const
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
             const int i = h2 + e;
-            const int u = min(u0 + i, n - 1);
+            const int u = u0 + i;                               // (rows past n - 1: in bounds, unused)
             const int guv = xch[i * 128 + v];                   // G_uv = (A B'^T)[u][v]
             const int auv = As[u * ld + v], buv = Bs[pu[e] * ld + px];
             dd[e] = 2 * (guv + (int)gv[e] - Dg[u] - dv + 2 * auv * buv);   // δ(u, v) (R10d)
@@ -413,11 +413,9 @@ __global__ void __launch_bounds__(tcs_nt<ENS>(), ENS ? 2 : 1) k_sa_scratch(const
         // (v >= n reads padding or the next row: in bounds, never used)
         const int dB = (int)Bs[pr * ld + px] - (int)Bs[ps * ld + px];
         const int ars = As[r * ld + s], brs = Bs[pr * ld + ps];
-        if (mma_pending) {                       // the previous update complete: tensor memory is current
-            if (!mma_done) tc::mbar_wait(mbar, ph);
-            ph ^= 1;
-            tc::fence_after_sync();
-        }
+        if (mma_pending & !mma_done) tc::mbar_wait(mbar, ph);
+        ph ^= (uint32_t)mma_pending;
+        tc::fence_after_sync();
         TCT_ACC(7, pt1, ph);
         uint32_t gps = 0, gpr = 0, g4[2], h4[2];   // PRE-update tensor memory
 #pragma unroll
