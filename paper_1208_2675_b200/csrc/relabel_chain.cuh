@@ -234,8 +234,7 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
         if (CL == 1) { D[e] = v; return; }
         const int g = e >> 2, own = g % CL;
         int32_t* loc = Ds + 4 * (g / CL) + (e & 3);
-        if (own == crank) *loc = v;
-        else cl_store(loc, own, v);
+        cl_store(loc, own, v);                            // (own rank too: no divergent branch)
     };
     bool pend_wait = false;                               // CL > 1: writes of the last update
     const NearSink sink{a.near_count, a.near_k, a.near_dec, a.near_cap, nullptr, nullptr, 0u};
@@ -421,7 +420,7 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
             for (int li = t; li < nql; li += RLB_NT) {
                 const uint32_t dsc = qdesc[li];
                 const int u = dsc & 511, v0 = (dsc >> 9) << 2;
-                if (u == sa || u == sb) continue;
+                const bool skip = (u == sa) | (u == sb);   // rows sa, sb: recomputed (R10b)
                 const int pu = stg[u];
                 const int4 x = *reinterpret_cast<const int4*>(stg + v0);
                 int4 o = D4[li];
@@ -436,9 +435,9 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
                 // columns sa, sb are the touching entries, stored (possibly by another CTA,
                 // unordered with this store) after the quads: leave them alone
                 const unsigned er = (unsigned)(sa - v0), es = (unsigned)(sb - v0);
-                if (er >= 4u && es >= 4u) {
+                if (!skip & (er >= 4u) & (es >= 4u)) {
                     D4[li] = o;
-                } else {
+                } else if (!skip) {
                     int32_t* q1 = Ds + 4 * li;
                     if (er != 0u && es != 0u) q1[0] = o.x;
                     if (er != 1u && es != 1u) q1[1] = o.y;
