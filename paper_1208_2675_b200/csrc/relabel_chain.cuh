@@ -287,13 +287,15 @@ __global__ void __launch_bounds__(RLB_NT, 1) k_sa_relabel(const RelabelArgs ra) 
 
         {   // thresholds of the window's iterations resident (theta_ring.cuh)
             const int ko = (int)(k - TR.kb);
-            if ((ko >> 8) != ring_blo) {      // a block passed (warp-uniform test; one thread refills)
-                ring_blo = ko >> 8;
-                if (t == 0) TR.refill(k);
-            }
-            if (ko + Wl > ring_hi) {
-                TR.ensure_ofs(ko + Wl);
-                ring_hi = (int)(TR.ready * RLB_RB);
+            if (((ko >> 8) != ring_blo) | (ko + Wl > ring_hi)) {   // one uniform branch for both rare cases
+                if ((ko >> 8) != ring_blo) {      // a block passed (warp-uniform test; one thread refills)
+                    ring_blo = ko >> 8;
+                    if (t == 0) TR.refill(k);
+                }
+                if (ko + Wl > ring_hi) {
+                    TR.ensure_ofs(ko + Wl);
+                    ring_hi = (int)(TR.ready * RLB_RB);
+                }
             }
         }
         if (CL > 1 && pend_wait) { cl_wait(); pend_wait = false; }   // other CTAs' updates visible
