@@ -171,14 +171,17 @@ __global__ void __launch_bounds__(E4_NT, 4) k_ens_scratch(const ChainArgs a, uns
         int Wl = win_f(R, L0, m1);
         if (W < Wl) Wl = W;
         if ((uint32_t)Wl > kr_end - kr) Wl = (int)(kr_end - kr);
-        if (t == 0)                              // blocks wholly below kr are consumed: free their slots
-            for (; ering_freed < (int)(kr / E4_EB); ++ering_freed) tc::mbar_arrive(ebar + NB + (ering_freed % NB));
-        if ((int)kr + Wl > ring_hi) {
-            while (ering_ready * E4_EB < (int)kr + Wl) {
-                tc::mbar_wait(ebar + (ering_ready % NB), (uint32_t)((ering_ready / NB) & 1));
-                ++ering_ready;
+        // the ring's rare cases behind one uniform branch (every thread counts the freed blocks)
+        if ((ering_freed < (int)(kr / E4_EB)) | ((int)kr + Wl > ring_hi)) {
+            for (; ering_freed < (int)(kr / E4_EB); ++ering_freed)   // blocks wholly below kr are consumed
+                if (t == 0) tc::mbar_arrive(ebar + NB + (ering_freed % NB));
+            if ((int)kr + Wl > ring_hi) {
+                while (ering_ready * E4_EB < (int)kr + Wl) {
+                    tc::mbar_wait(ebar + (ering_ready % NB), (uint32_t)((ering_ready / NB) & 1));
+                    ++ering_ready;
+                }
+                ring_hi = ering_ready * E4_EB;
             }
-            ring_hi = ering_ready * E4_EB;
         }
         // the window's rows of G to shared memory: the warp owning lane u_i reads whole lanes
         int pu[4];
